@@ -1,0 +1,208 @@
+/* dflow.h — C ABI of the B200-native replicated Relu(XW+b) MLP train step
+ * (arXiv 1603.04467, "TensorFlow: Large-Scale Machine Learning on
+ * Heterogeneous Distributed Systems").
+ *
+ * The calls follow the paper's statement of the problem:
+ *   1. build a dataflow graph of ops              PAPER.md §2 :159-185, Fig.1 :100-106
+ *   2. add its gradient graph                     PAPER.md §4.1 :494-518 ("[db,dW,dx] = tf.gradients(C,[b,W,x])" :512)
+ *   3. Run it with feeds and fetches              PAPER.md §2 :237-254, §4.2 :564-572
+ *   4. as a synchronously replicated train step   PAPER.md §7 :932-945 (Fig.7 top)
+ *      whose cross-device gradient transfers are compressed 32->16->32
+ *                                                 PAPER.md §5.5 :805-821
+ *
+ * Conventions (all functions):
+ *   - Return dflow_status; DFLOW_OK == 0.  No exception or abort crosses the ABI.
+ *     dflow_last_error() gives a thread-local message for the last failure.
+ *   - Pointers are plain host or device pointers; sizes are element counts.
+ *     Matrices are row-major with an explicit leading dimension (elements).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - A CUDA or NCCL failure inside a session poisons it: every later call on that
+ *     session returns DFLOW_SESSION_POISONED; destroy and recreate it (the paper's
+ *     "aborted and restarted").
+ *   - No CPU fallback: without a usable sm_100 GPU, compute entry points return
+ *     DFLOW_CUDA.  Graph-building entry points are host-only and need no GPU.
+ */
+#ifndef DFLOW_H_
+#define DFLOW_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t dflow_status;
+#define DFLOW_OK 0
+#define DFLOW_INVALID_ARGUMENT 1
+#define DFLOW_DUPLICATE_NAME 2      /* SPEC.md:122 add_node errors */
+#define DFLOW_UNKNOWN_OP 3
+#define DFLOW_DANGLING_INPUT 4
+#define DFLOW_SHAPE_MISMATCH 5
+#define DFLOW_NON_DIFFERENTIABLE 6  /* SPEC.md:358 add_gradients errors */
+#define DFLOW_NON_SCALAR_TARGET 7
+#define DFLOW_UNIMPLEMENTED 8       /* graph is not a chain the GPU planner can fuse */
+#define DFLOW_NOT_INITIALIZED 9
+#define DFLOW_CUDA 10
+#define DFLOW_NCCL 11
+#define DFLOW_OOM 12
+#define DFLOW_SESSION_POISONED 13
+#define DFLOW_BUFFER_TOO_SMALL 14
+
+/* Thread-local, valid until the next dflow_* call on this thread. */
+const char* dflow_last_error(void);
+/* Static string naming a status code, e.g. "DFLOW_SHAPE_MISMATCH". */
+const char* dflow_status_name(dflow_status s);
+/* Library version string. */
+const char* dflow_version(void);
+
+typedef enum { DFLOW_F32 = 1, DFLOW_BF16 = 7, DFLOW_U16 = 8 } dflow_dtype;
+typedef int32_t dflow_node; /* node id; every hot-path op has exactly one output (port 0) */
+typedef struct dflow_graph dflow_graph;
+typedef struct dflow_session dflow_session;
+
+#define DFLOW_BATCH (-1)   /* unknown (batch) dimension; only Placeholders may have it */
+#define DFLOW_LOSS_MSE 0   /* C = sum((a - y)^2) / (2 * rows * cols)   (reading A2) */
+#define DFLOW_LOSS_SUM 1   /* C = sum(a) / rows                        (reading A2) */
+
+/* ------------------------------------------------------------------ graph
+ * Host-only, caller-owned.  Node names match [A-Za-z0-9_./]+ and are unique.
+ * A failing call leaves the graph unchanged.              */
+dflow_status dflow_graph_create(dflow_graph** out);
+void dflow_graph_destroy(dflow_graph* g);
+dflow_status dflow_graph_num_nodes(const dflow_graph* g, int32_t* out);
+dflow_status dflow_node_by_name(const dflow_graph* g, const char* name, dflow_node* out);
+
+/* Placeholder: a fed input ("tf.placeholder"); dims may hold DFLOW_BATCH. */
+dflow_status dflow_placeholder(dflow_graph* g, const char* name, dflow_dtype dtype, int rank,
+                               const int64_t* dims, dflow_node* out);
+/* Variable: persistent mutable tensor; static dims. */
+dflow_status dflow_variable(dflow_graph* g, const char* name, dflow_dtype dtype, int rank,
+                            const int64_t* dims, dflow_node* out);
+/* MatMul(a, b) = op(a) op(b) (Table 1); rank-2 operands. */
+dflow_status dflow_matmul(dflow_graph* g, const char* name, dflow_node a, dflow_node b, int transpose_a,
+                          int transpose_b, dflow_node* out);
+/* Add(a, b): same shapes, or b rank-1 broadcast over the rows of a (BiasAdd, Fig.1 "Wx+b"). */
+dflow_status dflow_add(dflow_graph* g, const char* name, dflow_node a, dflow_node b, dflow_node* out);
+/* Relu(x) = max(x, 0). */
+dflow_status dflow_relu(dflow_graph* g, const char* name, dflow_node x, dflow_node* out);
+/* Scalar cost C ("C = [...]"; reading A2).  target = -1 for DFLOW_LOSS_SUM. */
+dflow_status dflow_loss(dflow_graph* g, const char* name, int kind, dflow_node pred, dflow_node target,
+                        dflow_node* out);
+/* Gradient graph: appends one gradient-function node per op on
+ * the paths xs -> cost, named grad/<forward-name>/<suffix>, partials summed by AddN,
+ * ZerosLike for sources C does not depend on.  out_grads[i] = dC/dxs[i].        */
+dflow_status dflow_gradients(dflow_graph* g, dflow_node cost, int n, const dflow_node* xs,
+                             dflow_node* out_grads);
+/* ApplyGradientDescent: var <- var - lr * grad. */
+dflow_status dflow_apply_gradient_descent(dflow_graph* g, const char* name, dflow_node var, float lr,
+                                          dflow_node grad, dflow_node* out);
+/* JSON {"version":1,"nodes":[{name, op, inputs, attrs, dtype, shape}]}.  Writes at
+ * most cap bytes (NUL-terminated); *needed = full length + 1.  Returns
+ * DFLOW_BUFFER_TOO_SMALL if cap < *needed. */
+dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, size_t* needed);
+
+/* ---------------------------------------------------------------- session
+ * One session per (rank, GPU).  dflow_session_create copies the graph (an
+ * immutable snapshot), runs the replication + compression-insertion pass and
+ * the planner (matches MatMul->Add->Relu chains + loss + gradient graph onto
+ * fused kernels; any unmatched node -> DFLOW_UNIMPLEMENTED), allocates all
+ * device state on `device`, and (world > 1) initialises NCCL from nccl_id.   */
+#define DFLOW_PRECISION_BF16 0    /* bf16 operands, fp32 accumulate/master weights (reading A13) */
+#define DFLOW_PRECISION_3XTF32 1  /* fp32-faithful 3xTF32 split (reading A14)                      */
+#define DFLOW_EXCHANGE_TRUNC16 0  /* alltoall(u16) + owner fold + allgather(u16) (readings A5-A7) */
+#define DFLOW_EXCHANGE_FP32 1     /* same schedule with fp32 payloads (deterministic)              */
+#define DFLOW_EXCHANGE_FP32_NCCL 2 /* ncclAllReduce(sum, fp32) then x 1/N (library baseline)        */
+#define DFLOW_EXCHANGE_NONE 3     /* debug/timing only: no exchange (N>1 results are wrong)        */
+
+typedef struct {
+  int32_t world;          /* N replicas (one process or thread per GPU)                      */
+  int32_t rank;           /* this replica, 0..N-1; gets rows [rank*b, (rank+1)*b) (reading A4) */
+  int32_t device;         /* CUDA device ordinal                                              */
+  int32_t precision;      /* DFLOW_PRECISION_*                                                */
+  int32_t exchange;       /* DFLOW_EXCHANGE_*                                                 */
+  int32_t overlap;        /* 1: per-layer exchange on a comm stream overlapped with backward  */
+  int32_t sm_reserve;     /* SMs left free by the GEMMs for concurrent NCCL kernels          */
+  int64_t max_local_rows; /* capacity b_max of every activation buffer                        */
+} dflow_options;
+
+/* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */
+dflow_status dflow_nccl_unique_id(uint8_t* out128);
+dflow_status dflow_session_create(const dflow_graph* g, const dflow_options* opt, const uint8_t* nccl_id128,
+                                  dflow_session** out);
+void dflow_session_destroy(dflow_session* s);
+/* JSON of the rewritten graph the session executes (after the compression pass). */
+dflow_status dflow_session_graph_to_json(const dflow_session* s, char* buf, size_t cap, size_t* needed);
+
+/* Variables: fp32 [dims] row-major, dense.  src/dst on host (flag 0) or device (1).
+ * Assign also refreshes the bf16 working copy.  Stream-ordered on `stream`;
+ * host copies are synchronous.                                                */
+dflow_status dflow_variable_assign(dflow_session* s, dflow_node var, const void* src, int src_on_device,
+                                   void* stream);
+dflow_status dflow_variable_read(dflow_session* s, dflow_node var, void* dst, int dst_on_device, void* stream);
+
+/* Run(targets = all ApplyGradientDescent nodes, fetch = C, feeds) on this rank's
+ * shard: forward, gradient graph, compressed exchange, update.  feeds[i] is a
+ * Placeholder; dev_ptrs[i] its device data (fp32 or bf16 per the placeholder's
+ * dtype) [local_rows, ld[i]], borrowed and stream-ordered on `stream`.
+ * local_rows = B / N.  loss_out (host) receives C = mean_r C_r after an internal
+ * sync; NULL = no host sync.                                                  */
+dflow_status dflow_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* dev_ptrs,
+                              const int64_t* ld, int64_t local_rows, float* loss_out, void* stream);
+/* Same, with HOST feed buffers (pinned for async copies): copies in, steps, and
+ * reads the loss back — the end-to-end path.                                  */
+dflow_status dflow_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                   const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
+                                   float* loss_out, void* stream);
+/* Fig.1 "s.run(C, feed_dict={x: input})": forward only, no update.  fetch is a
+ * Relu node (writes fp32 [local_rows, out] dense) or the cost (writes 1 fp32). */
+dflow_status dflow_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* dev_ptrs,
+                           const int64_t* ld, int64_t local_rows, dflow_node fetch, void* out_dev, void* stream);
+/* Fetch gradient nodes (fp32, dense, shapes as in the graph, batch = local_rows)
+ * without exchange or update (Fig.5: [db, dW, dx]).                           */
+dflow_status dflow_fetch_gradients(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                   const void* const* dev_ptrs, const int64_t* ld, int64_t local_rows, int n,
+                                   const dflow_node* grads, void* const* out_dev, void* stream);
+/* Masks 1[A_l > 0] of layer `layer` (1-based) from the most recent forward on
+ * this rank, bit-packed row-major (bit i of word i/32), ceil(rows*out/32) words,
+ * written to HOST memory.  Input to the oracle's mask-locked mode (reading A22). */
+dflow_status dflow_fetch_relu_masks(dflow_session* s, int layer, uint32_t* out_bits_host);
+
+typedef struct {
+  int32_t launches_per_step; /* dflow kernels launched by one dflow_train_step     */
+  int32_t gemm_launches_per_step;
+  int32_t layers;
+  int32_t nonfinite;         /* non-finite guard: last step's loss was NaN/Inf */
+  double gemm_ms;            /* accumulated device time of GEMM launches (timing on) */
+  double other_ms;           /* accumulated device time of the other kernels       */
+  double exchange_ms;        /* accumulated device time of the exchange            */
+  int64_t timed_steps;
+  double gemm_flops_per_step; /* algorithmic GEMM FLOPs of one step on this rank    */
+} dflow_stats;
+/* Per-kernel CUDA-event timing inside dflow_train_step (off by default). */
+dflow_status dflow_session_set_timing(dflow_session* s, int enable);
+dflow_status dflow_session_stats(dflow_session* s, dflow_stats* out);
+
+/* ------------------------------------------------------- standalone ops
+ * Bit-exact codec (reading A5): dst[i] = bits(src[i]) >> 16,
+ * and dst[i] = float(bits = src[i] << 16).  Device pointers, n elements.       */
+dflow_status dflow_truncate16(const float* src, uint16_t* dst, size_t n, void* stream);
+dflow_status dflow_expand16(const uint16_t* src, float* dst, size_t n, void* stream);
+/* Exchange alone (a6-a8) on this session's communicator: grad_dev fp32 [n] on
+ * every rank -> out_dev fp32 [n] = the g_hat every replica applies.           */
+dflow_status dflow_exchange(dflow_session* s, const float* grad_dev, float* out_dev, size_t n, void* stream);
+/* One GEMM through the tcgen05 kernel family (layout/epilogue unit tests):
+ *   C[m,n] = sum_k A(m,k) B(k,n);  a_mn=0: A(m,k)=A[m*lda+k], 1: A[k*lda+m];
+ *   b_mn=0: B(k,n)=B[n*ldb+k], 1: B[k*ldb+n]; bf16 operands, lda/ldb % 8 == 0.
+ *   epilogue 0: out_f32 = acc; 1: out (u16) = bits(acc)>>16;
+ *   2: relu(acc + bias) -> out (bf16) and/or out_f32; 3: out (bf16) = acc*1[mask>0].
+ *   tile 0 auto, 1 = 128x128 single CTA, 2 = 256x256 CTA pair.                 */
+dflow_status dflow_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int a_mn, const void* B,
+                             int64_t ldb, int b_mn, int epilogue, void* out, int64_t ldo, float* out_f32,
+                             int64_t ldo32, const float* bias, const void* mask, int64_t ldm, int tile,
+                             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFLOW_H_ */

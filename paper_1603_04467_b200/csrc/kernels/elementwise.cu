@@ -1,0 +1,496 @@
+// HBM-bound kernels of the replicated MLP step (NK7-NK13).  Vectorised 16-byte
+// loads/stores, grid-stride loops sized to a few waves of 148 SMs, explicit
+// round-to-nearest intrinsics (no FMA contraction, no flush-to-zero) wherever the
+// oracle fixes the bits (codec, owner fold, SGD update).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "elementwise.h"
+
+namespace dflow {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kMaxBlocks = 148 * 8;
+
+inline int blocks_for(int64_t work_items) {
+  int64_t b = (work_items + kThreads - 1) / kThreads;
+  if (b < 1) b = 1;
+  return static_cast<int>(std::min<int64_t>(b, kMaxBlocks));
+}
+
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+__device__ __forceinline__ uint32_t pack2_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// ------------------------------------------------------------------ codec
+__global__ void k_truncate16(const float* __restrict__ src, uint16_t* __restrict__ dst, int64_t n, int vec) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / 8;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int64_t i = tid; i < nv; i += stride) {
+      const uint4 a = s4[2 * i], b = s4[2 * i + 1];
+      uint4 o;
+      o.x = (a.x >> 16) | (a.y & 0xFFFF0000u);
+      o.y = (a.z >> 16) | (a.w & 0xFFFF0000u);
+      o.z = (b.x >> 16) | (b.y & 0xFFFF0000u);
+      o.w = (b.z >> 16) | (b.w & 0xFFFF0000u);
+      d4[i] = o;
+    }
+    done = nv * 8;
+  }
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+  for (int64_t i = done + tid; i < n; i += stride) dst[i] = static_cast<uint16_t>(s[i] >> 16);
+}
+
+__global__ void k_expand16(const uint16_t* __restrict__ src, float* __restrict__ dst, int64_t n, int vec) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t done = 0;
+  if (vec) {
+    const int64_t nv = n / 8;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int64_t i = tid; i < nv; i += stride) {
+      const uint4 q = s4[i];
+      d4[2 * i] = make_uint4(q.x << 16, q.x & 0xFFFF0000u, q.y << 16, q.y & 0xFFFF0000u);
+      d4[2 * i + 1] = make_uint4(q.z << 16, q.z & 0xFFFF0000u, q.w << 16, q.w & 0xFFFF0000u);
+    }
+    done = nv * 8;
+  }
+  uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+  for (int64_t i = done + tid; i < n; i += stride) d[i] = static_cast<uint32_t>(src[i]) << 16;
+}
+
+// ------------------------------------------------------------------ casts
+__global__ void k_cast_bf16(const float* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
+                            int64_t ldd, int64_t rows, int64_t cols, int vec) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {  // cols % 8 == 0, aligned rows
+    const int64_t per_row = cols / 8, total = rows * per_row;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int64_t r = i / per_row, c = (i - r * per_row) * 8;
+      const float4 a = *reinterpret_cast<const float4*>(src + r * lds + c);
+      const float4 b = *reinterpret_cast<const float4*>(src + r * lds + c + 4);
+      *reinterpret_cast<uint4*>(dst + r * ldd + c) =
+          make_uint4(pack2_bf16(a.x, a.y), pack2_bf16(a.z, a.w), pack2_bf16(b.x, b.y), pack2_bf16(b.z, b.w));
+    }
+  } else {
+    const int64_t total = rows * cols;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int64_t r = i / cols, c = i - r * cols;
+      dst[r * ldd + c] = __float2bfloat16_rn(src[r * lds + c]);
+    }
+  }
+}
+
+__global__ void k_copy_bf16(const __nv_bfloat16* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
+                            int64_t ldd, int64_t rows, int64_t cols) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t total = rows * cols;
+  for (int64_t i = tid; i < total; i += stride) {
+    const int64_t r = i / cols, c = i - r * cols;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+}
+
+__global__ void k_bf16_to_f32(const __nv_bfloat16* __restrict__ a, int64_t ld, int64_t rows, int64_t cols,
+                              float* __restrict__ out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < rows * cols; i += stride) {
+    const int64_t r = i / cols, c = i - r * cols;
+    out[i] = __bfloat162float(a[r * ld + c]);
+  }
+}
+
+__global__ void k_copy_f32(const float* __restrict__ a, int64_t lds, int64_t rows, int64_t cols,
+                           float* __restrict__ out, int64_t ldd) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < rows * cols; i += stride) {
+    const int64_t r = i / cols, c = i - r * cols;
+    out[r * ldd + c] = a[r * lds + c];
+  }
+}
+
+// ------------------------------------------------------------------ loss
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One block per row slice (grid-stride over rows); each thread walks columns.
+__global__ void k_loss_seed(int kind, const float* __restrict__ a, int64_t lda, const float* __restrict__ y,
+                            int64_t ldy, int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ dz, int64_t lddz,
+                            float* __restrict__ dz32, int64_t lddz32, double* __restrict__ partials) {
+  const float denom = static_cast<float>(rows * cols);
+  const float inv_rows = __fdiv_rn(1.0f, static_cast<float>(rows));
+  double acc = 0.0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float av = a[r * lda + c];
+      float g;
+      if (kind == 0) {
+        const float d = __fsub_rn(av, y[r * ldy + c]);
+        acc += static_cast<double>(d) * static_cast<double>(d);
+        g = __fdiv_rn(d, denom);  // IEEE division (reading A20)
+      } else {
+        acc += static_cast<double>(av);
+        g = inv_rows;
+      }
+      const float v = (av > 0.f) ? g : 0.f;  // Relu'(a) with Relu'(0) = 0 (reading A10)
+      if (dz) dz[r * lddz + c] = __float2bfloat16_rn(v);
+      if (dz32) dz32[r * lddz32 + c] = v;
+    }
+  }
+  __shared__ double sm[32];
+  acc = warp_sum_d(acc);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = (threadIdx.x < (blockDim.x >> 5)) ? sm[threadIdx.x] : 0.0;
+    v = warp_sum_d(v);
+    if (threadIdx.x == 0) partials[blockIdx.x] = v;
+  }
+}
+
+__global__ void k_loss_final(int kind, const double* __restrict__ partials, int n, int64_t rows, int64_t cols,
+                             float* __restrict__ loss) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) v += partials[i];
+  v = warp_sum_d(v);
+  if (threadIdx.x == 0) {
+    const double c = (kind == 0) ? v / (2.0 * static_cast<double>(rows) * static_cast<double>(cols))
+                                 : v / static_cast<double>(rows);
+    *loss = static_cast<float>(c);
+  }
+}
+
+// ------------------------------------------------------------------ colsum
+// Block (x = 256-column slab, y = row chunk); thread = 8 consecutive columns x one of 8 row lanes.
+template <typename T>
+__global__ void k_colsum_partial(const T* __restrict__ dz, int64_t ld, int64_t rows, int64_t cols,
+                                 int64_t rows_per_chunk, float* __restrict__ ws, int vec) {
+  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
+  const int64_t c0 = blockIdx.x * 256 + cg * 8;
+  const int64_t r0 = blockIdx.y * rows_per_chunk;
+  const int64_t r1 = min(rows, r0 + rows_per_chunk);
+  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const bool full = vec && (c0 + 8 <= cols);
+  for (int64_t r = r0 + rl; r < r1; r += 8) {
+    const T* p = dz + r * ld + c0;
+    if constexpr (sizeof(T) == 2) {
+      if (full) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16));
+        continue;
+      }
+    } else {
+      if (full) {
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        const float4 b = *reinterpret_cast<const float4*>(p + 4);
+        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], v[e]);
+        continue;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (c0 + e < cols) {
+        float x;
+        if constexpr (sizeof(T) == 2) x = __bfloat162float(p[e]); else x = p[e];
+        s[e] = __fadd_rn(s[e], x);
+      }
+  }
+  __shared__ float sm[8][256 + 8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sm[rl][cg * 8 + e] = s[e];
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (blockIdx.x * 256 + c < cols) {
+    float t = sm[0][c];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t = __fadd_rn(t, sm[k][c]);
+    ws[blockIdx.y * cols + blockIdx.x * 256 + c] = t;
+  }
+}
+
+__global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols, float* __restrict__ out32,
+                               uint16_t* __restrict__ out16) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+    float t = ws[c];
+    for (int k = 1; k < chunks; ++k) t = __fadd_rn(t, ws[k * cols + c]);
+    if (out32) out32[c] = t;
+    if (out16) out16[c] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
+  }
+}
+
+// ------------------------------------------------------------------ owner reduce
+__global__ void k_owner_reduce_t16(const uint16_t* __restrict__ recv, int64_t shard, int nranks,
+                                   uint16_t* __restrict__ out) {
+  const float inv = 1.0f / static_cast<float>(nranks);  // exact for power-of-two N (reading A7)
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nv = shard / 8;  // shard is a multiple of 8 (bucket padding)
+  for (int64_t i = tid; i < nv; i += stride) {
+    float s[8];
+    {
+      const uint4 q = reinterpret_cast<const uint4*>(recv)[i];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16);
+    }
+    for (int r = 1; r < nranks; ++r) {  // left fold in rank order
+      const uint4 q = reinterpret_cast<const uint4*>(recv + r * shard)[i];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16));
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const uint32_t lo = __float_as_uint(__fmul_rn(s[e], inv)) >> 16;
+      const uint32_t hi = __float_as_uint(__fmul_rn(s[e + 1], inv)) & 0xFFFF0000u;
+      o[e >> 1] = lo | hi;
+    }
+    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__global__ void k_owner_reduce_f32(const float* __restrict__ recv, int64_t shard, int nranks,
+                                   float* __restrict__ out) {
+  const float inv = 1.0f / static_cast<float>(nranks);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < shard; i += stride) {
+    float s = recv[i];
+    for (int r = 1; r < nranks; ++r) s = __fadd_rn(s, recv[r * shard + i]);
+    out[i] = __fmul_rn(s, inv);
+  }
+}
+
+__global__ void k_scale_f32(float* __restrict__ x, int64_t n, float scale) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < n; i += stride) x[i] = __fmul_rn(x[i], scale);
+}
+
+// ------------------------------------------------------------------ SGD apply
+__device__ __forceinline__ float sgd(float w, float lr, float g) { return __fsub_rn(w, __fmul_rn(lr, g)); }
+
+__global__ void k_apply_sgd_vec(float* __restrict__ W, const float* __restrict__ g32,
+                                const uint16_t* __restrict__ g16, int64_t n8, __nv_bfloat16* __restrict__ wbf,
+                                float lr) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < n8; i += stride) {
+    float4 w0 = reinterpret_cast<float4*>(W)[2 * i], w1 = reinterpret_cast<float4*>(W)[2 * i + 1];
+    float g[8];
+    if (g16) {
+      const uint4 q = reinterpret_cast<const uint4*>(g16)[i];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) g[e] = __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16);
+    } else {
+      const float4 a = reinterpret_cast<const float4*>(g32)[2 * i], b = reinterpret_cast<const float4*>(g32)[2 * i + 1];
+      g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w; g[4] = b.x; g[5] = b.y; g[6] = b.z; g[7] = b.w;
+    }
+    w0.x = sgd(w0.x, lr, g[0]); w0.y = sgd(w0.y, lr, g[1]); w0.z = sgd(w0.z, lr, g[2]); w0.w = sgd(w0.w, lr, g[3]);
+    w1.x = sgd(w1.x, lr, g[4]); w1.y = sgd(w1.y, lr, g[5]); w1.z = sgd(w1.z, lr, g[6]); w1.w = sgd(w1.w, lr, g[7]);
+    reinterpret_cast<float4*>(W)[2 * i] = w0;
+    reinterpret_cast<float4*>(W)[2 * i + 1] = w1;
+    if (wbf)
+      reinterpret_cast<uint4*>(wbf)[i] = make_uint4(pack2_bf16(w0.x, w0.y), pack2_bf16(w0.z, w0.w),
+                                                    pack2_bf16(w1.x, w1.y), pack2_bf16(w1.z, w1.w));
+  }
+}
+
+__global__ void k_apply_sgd(float* __restrict__ W, const float* __restrict__ g32, const uint16_t* __restrict__ g16,
+                            int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ wbf, int64_t ldwb, float lr) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = rows * cols;
+  for (int64_t i = tid; i < n; i += stride) {
+    const float g = g16 ? __uint_as_float(static_cast<uint32_t>(g16[i]) << 16) : g32[i];
+    const float w = sgd(W[i], lr, g);
+    W[i] = w;
+    if (wbf) {
+      const int64_t r = i / cols, c = i - r * cols;
+      wbf[r * ldwb + c] = __float2bfloat16_rn(w);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ masks
+template <typename T>
+__global__ void k_relu_mask_bits(const T* __restrict__ a, int64_t ld, int64_t rows, int64_t cols,
+                                 uint32_t* __restrict__ bits) {
+  const int64_t n = rows * cols;
+  const int64_t words = (n + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w < words; w += nwarps) {
+    const int64_t i = w * 32 + lane;
+    bool p = false;
+    if (i < n) {
+      const int64_t r = i / cols, c = i - r * cols;
+      float v;
+      if constexpr (sizeof(T) == 2) v = __bfloat162float(a[r * ld + c]); else v = a[r * ld + c];
+      p = v > 0.f;
+    }
+    const uint32_t b = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) bits[w] = b;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_truncate16(const float* src, uint16_t* dst, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int vec = al16(src) && al16(dst);
+  k_truncate16<<<blocks_for(vec ? (int64_t)n / 8 : (int64_t)n), kThreads, 0, s>>>(src, dst, (int64_t)n, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_expand16(const uint16_t* src, float* dst, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int vec = al16(src) && al16(dst);
+  k_expand16<<<blocks_for(vec ? (int64_t)n / 8 : (int64_t)n), kThreads, 0, s>>>(src, dst, (int64_t)n, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cast_bf16(const float* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
+                             int64_t cols, cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  const int vec = (cols % 8 == 0) && (lds % 4 == 0) && (ldd % 8 == 0) && al16(src) && al16(dst);
+  k_cast_bf16<<<blocks_for(vec ? rows * cols / 8 : rows * cols), kThreads, 0, s>>>(src, lds, dst, ldd, rows, cols,
+                                                                                  vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
+                             int64_t cols, cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  k_copy_bf16<<<blocks_for(rows * cols), kThreads, 0, s>>>(src, lds, dst, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_seed(int kind, const float* a, int64_t lda, const float* y, int64_t ldy, int64_t rows,
+                             int64_t cols, __nv_bfloat16* dz, int64_t lddz, float* dz32, int64_t lddz32,
+                             double* partials, float* loss_dev, cudaStream_t s) {
+  k_loss_seed<<<kLossBlocks, kThreads, 0, s>>>(kind, a, lda, y, ldy, rows, cols, dz, lddz, dz32, lddz32, partials);
+  k_loss_final<<<1, 32, 0, s>>>(kind, partials, kLossBlocks, rows, cols, loss_dev);
+  return cudaGetLastError();
+}
+
+int colsum_rowchunks(int64_t rows, int64_t cols) {
+  const int64_t slabs = (cols + 255) / 256;
+  int64_t chunks = (148 * 4 + slabs - 1) / slabs;
+  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, (rows + 63) / 64));
+  return static_cast<int>(std::max<int64_t>(chunks, 1));
+}
+
+template <typename T>
+static cudaError_t colsum_impl(const T* dz, int64_t ld, int64_t rows, int64_t cols, float* ws, float* out_f32,
+                               uint16_t* out_u16, cudaStream_t s) {
+  if (cols == 0) return cudaSuccess;
+  const int chunks = colsum_rowchunks(rows, cols);
+  const int64_t rpc = (rows + chunks - 1) / chunks;
+  const int vec = al16(dz) && ((ld * (int64_t)sizeof(T)) % 16 == 0);
+  dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>(chunks));
+  k_colsum_partial<T><<<grid, 256, 0, s>>>(dz, ld, rows, cols, rpc > 0 ? rpc : 1, ws, vec);
+  k_colsum_final<<<blocks_for(cols), kThreads, 0, s>>>(ws, chunks, cols, out_f32, out_u16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int64_t ld, int64_t rows, int64_t cols, float* ws,
+                               float* out_f32, uint16_t* out_u16, cudaStream_t s) {
+  return colsum_impl(dz, ld, rows, cols, ws, out_f32, out_u16, s);
+}
+
+cudaError_t launch_colsum_f32(const float* dz, int64_t ld, int64_t rows, int64_t cols, float* ws, float* out_f32,
+                              uint16_t* out_u16, cudaStream_t s) {
+  return colsum_impl(dz, ld, rows, cols, ws, out_f32, out_u16, s);
+}
+
+cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,
+                                    cudaStream_t s) {
+  if (shard == 0) return cudaSuccess;
+  k_owner_reduce_t16<<<blocks_for(shard / 8), kThreads, 0, s>>>(recv, shard, nranks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_owner_reduce_f32(const float* recv, int64_t shard, int nranks, float* out, cudaStream_t s) {
+  if (shard == 0) return cudaSuccess;
+  k_owner_reduce_f32<<<blocks_for(shard), kThreads, 0, s>>>(recv, shard, nranks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_f32(float* x, int64_t n, float scale, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_scale_f32<<<blocks_for(n), kThreads, 0, s>>>(x, n, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_sgd(float* W, const float* g32, const uint16_t* g16, int64_t rows, int64_t cols,
+                             __nv_bfloat16* wbf, int64_t ldwb, float lr, cudaStream_t s) {
+  const int64_t n = rows * cols;
+  if (n == 0) return cudaSuccess;
+  const bool dense = (wbf == nullptr) || (ldwb == cols);
+  const bool vec = dense && (n % 8 == 0) && al16(W) && (g16 ? al16(g16) : al16(g32)) && (!wbf || al16(wbf));
+  if (vec)
+    k_apply_sgd_vec<<<blocks_for(n / 8), kThreads, 0, s>>>(W, g32, g16, n / 8, wbf, lr);
+  else
+    k_apply_sgd<<<blocks_for(n), kThreads, 0, s>>>(W, g32, g16, rows, cols, wbf, ldwb, lr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relu_mask_bits(const __nv_bfloat16* a, int64_t ld, int64_t rows, int64_t cols, uint32_t* bits,
+                                  cudaStream_t s) {
+  const int64_t n = rows * cols;
+  if (n == 0) return cudaSuccess;
+  k_relu_mask_bits<__nv_bfloat16><<<blocks_for(n), kThreads, 0, s>>>(a, ld, rows, cols, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relu_mask_bits_f32(const float* a, int64_t ld, int64_t rows, int64_t cols, uint32_t* bits,
+                                      cudaStream_t s) {
+  const int64_t n = rows * cols;
+  if (n == 0) return cudaSuccess;
+  k_relu_mask_bits<float><<<blocks_for(n), kThreads, 0, s>>>(a, ld, rows, cols, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bf16_to_f32(const __nv_bfloat16* a, int64_t ld, int64_t rows, int64_t cols, float* out,
+                               cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  k_bf16_to_f32<<<blocks_for(rows * cols), kThreads, 0, s>>>(a, ld, rows, cols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_f32(const float* a, int64_t lds, int64_t rows, int64_t cols, float* out, int64_t ldd,
+                            cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  k_copy_f32<<<blocks_for(rows * cols), kThreads, 0, s>>>(a, lds, rows, cols, out, ldd);
+  return cudaGetLastError();
+}
+
+}  // namespace dflow

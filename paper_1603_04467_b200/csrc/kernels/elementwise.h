@@ -1,0 +1,63 @@
+// HBM-bound kernels of the step (NK7-NK13): codec, loss seed, bias-gradient
+// column sum, owner reduce, SGD apply, casts, relu masks.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dflow {
+
+// NK9 / NK10: dst[i] = bits(src[i]) >> 16  /  dst[i] = float(bits = src[i] << 16)
+cudaError_t launch_truncate16(const float* src, uint16_t* dst, size_t n, cudaStream_t s);
+cudaError_t launch_expand16(const uint16_t* src, float* dst, size_t n, cudaStream_t s);
+
+// NK13: dst bf16 [rows, ldd] = RNE(src f32 [rows, lds]) for cols columns.
+cudaError_t launch_cast_bf16(const float* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
+                             int64_t cols, cudaStream_t s);
+// bf16 [rows, lds] -> bf16 [rows, ldd] (bf16 feeds with a foreign leading dim).
+cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
+                             int64_t cols, cudaStream_t s);
+
+// NK7: loss and gradient seed from the last activation a (fp32).
+//   MSE: d = a - y;  dz = 1[a>0] * d / (rows*cols);  C = sum(d^2) / (2 rows cols)
+//   SUM:             dz = 1[a>0] * (1 / rows);       C = sum(a) / rows
+// Writes dz (bf16) and/or dz32 (fp32); the loss lands in *loss_dev (fp32) via
+// a deterministic two-pass reduction (fixed grid, fixed order).
+constexpr int kLossBlocks = 296;
+cudaError_t launch_loss_seed(int kind, const float* a, int64_t lda, const float* y, int64_t ldy, int64_t rows,
+                             int64_t cols, __nv_bfloat16* dz, int64_t lddz, float* dz32, int64_t lddz32,
+                             double* partials /*[kLossBlocks]*/, float* loss_dev, cudaStream_t s);
+
+// NK8: db[c] = sum_r dz[r, c] (bf16 input, fp32 accumulate, fixed order).
+// Outputs fp32 and/or trunc16 (u16).  ws: rowchunks*cols floats scratch.
+int colsum_rowchunks(int64_t rows, int64_t cols);
+cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int64_t ld, int64_t rows, int64_t cols, float* ws,
+                               float* out_f32, uint16_t* out_u16, cudaStream_t s);
+cudaError_t launch_colsum_f32(const float* dz, int64_t ld, int64_t rows, int64_t cols, float* ws, float* out_f32,
+                              uint16_t* out_u16, cudaStream_t s);
+
+// NK11: owner fold of N received shards (rank order), x (1/N), truncate.
+cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,
+                                    cudaStream_t s);
+cudaError_t launch_owner_reduce_f32(const float* recv, int64_t shard, int nranks, float* out, cudaStream_t s);
+// x (1/N) in place (FP32_NCCL after an allreduce-sum).
+cudaError_t launch_scale_f32(float* x, int64_t n, float scale, cudaStream_t s);
+
+// NK12: W <- fl(W - fl(lr * g)); g from fp32 (g32) or expanded u16 (g16).
+// W dense [n = rows*cols]; optional bf16 working copy wbf [rows, ldwb].
+cudaError_t launch_apply_sgd(float* W, const float* g32, const uint16_t* g16, int64_t rows, int64_t cols,
+                             __nv_bfloat16* wbf, int64_t ldwb, float lr, cudaStream_t s);
+
+// Bit-pack 1[a > 0] of a bf16 [rows, ld] activation (cols columns) row-major.
+cudaError_t launch_relu_mask_bits(const __nv_bfloat16* a, int64_t ld, int64_t rows, int64_t cols, uint32_t* bits,
+                                  cudaStream_t s);
+cudaError_t launch_relu_mask_bits_f32(const float* a, int64_t ld, int64_t rows, int64_t cols, uint32_t* bits,
+                                      cudaStream_t s);
+// bf16 [rows, ld] -> dense fp32 [rows, cols]
+cudaError_t launch_bf16_to_f32(const __nv_bfloat16* a, int64_t ld, int64_t rows, int64_t cols, float* out,
+                               cudaStream_t s);
+// fp32 [rows, lds] -> dense fp32 [rows, cols]
+cudaError_t launch_copy_f32(const float* a, int64_t lds, int64_t rows, int64_t cols, float* out, int64_t ldd,
+                            cudaStream_t s);
+
+}  // namespace dflow

@@ -1,0 +1,176 @@
+// Host launcher for the tcgen05 GEMM family (NK1-NK3): TMA descriptor
+// encoding, tile-config choice, persistent grid sizing, cluster launch.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "gemm.cuh"
+#include "gemm.h"
+
+namespace dflow {
+
+static thread_local char g_err[512];
+const char* gemm_last_error() { return g_err; }
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major matrix with `inner` contiguous elements
+// per row (logical extent), `outer` rows, row pitch `ld` elements.
+static bool make_tmap_bf16(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ld,
+                           uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 2) & 15)) {
+    snprintf(g_err, sizeof g_err, "TMA needs 16-byte aligned base and row pitch (ld=%lld)", (long long)ld);
+    return false;
+  }
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%u,%u",
+             (int)r, (long long)inner, (long long)outer, (long long)ld, box_inner, box_outer);
+    return false;
+  }
+  return true;
+}
+
+template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
+static void* kernel_ptr() {
+  auto k = &gemm_bf16_kernel<BN, CG, A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, CG>::SMEM_BYTES);
+    attr_set = true;
+  }
+  return reinterpret_cast<void*>(k);
+}
+
+template <int BN, int CG>
+static void* select_kernel(bool a_mn, bool b_mn, int epi) {
+  if (!a_mn && b_mn) {
+    if (epi == EPI_BIAS_RELU) return kernel_ptr<BN, CG, false, true, EPI_BIAS_RELU>();
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, false, true, EPI_F32>();
+  } else if (!a_mn && !b_mn) {
+    if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, false, false, EPI_RELUGRAD>();
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, false, false, EPI_F32>();
+  } else if (a_mn && b_mn) {
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, true, true, EPI_F32>();
+    if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, true, true, EPI_TRUNC16>();
+  }
+  return nullptr;
+}
+
+static bool aligned16(const void* p, int64_t ld, int elem) {
+  return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ((ld * elem) & 15) == 0;
+}
+
+cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
+  g_err[0] = 0;
+  if (d.M <= 0 || d.N <= 0 || d.K < 0 || d.M > (1 << 30) || d.N > (1 << 30) || d.K > (1 << 30)) {
+    snprintf(g_err, sizeof g_err, "bad GEMM shape %lld x %lld x %lld", (long long)d.M, (long long)d.N, (long long)d.K);
+    return cudaErrorInvalidValue;
+  }
+  int tile = d.tile;
+  if (tile == 0) {
+    const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
+    tile = (pair_tiles >= num_sms / 2) ? 2 : 1;
+  }
+  const int BN = (tile == 2) ? 256 : 128;
+  const int CG = (tile == 2) ? 2 : 1;
+  const int BN_CTA = BN / CG;
+  plan->d = d;
+  plan->tile = tile;
+  plan->cluster = CG;
+  plan->tiles_m = static_cast<int>((d.M + 128 * CG - 1) / (128 * CG));
+  plan->tiles_n = static_cast<int>((d.N + BN - 1) / BN);
+  void* k = (tile == 2) ? select_kernel<256, 2>(d.a_mn, d.b_mn, d.epilogue)
+                        : select_kernel<128, 1>(d.a_mn, d.b_mn, d.epilogue);
+  if (!k) {
+    snprintf(g_err, sizeof g_err, "unsupported GEMM layout/epilogue (a_mn=%d b_mn=%d epi=%d)", d.a_mn, d.b_mn,
+             d.epilogue);
+    return cudaErrorInvalidValue;
+  }
+  plan->kernel = k;
+  plan->smem = (tile == 2) ? GemmCfg<256, 2>::SMEM_BYTES : GemmCfg<128, 1>::SMEM_BYTES;
+  const int64_t K = d.K > 0 ? d.K : 1;
+  bool ok = d.a_mn ? make_tmap_bf16(&plan->tmA, d.A, d.M, K, d.lda, 64, 64)
+                   : make_tmap_bf16(&plan->tmA, d.A, K, d.M, d.lda, 64, 128);
+  ok = ok && (d.b_mn ? make_tmap_bf16(&plan->tmB, d.B, d.N, K, d.ldb, 64, 64)
+                     : make_tmap_bf16(&plan->tmB, d.B, K, d.N, d.ldb, 64, BN_CTA));
+  if (!ok) return cudaErrorInvalidValue;
+  GemmArgs& a = plan->args;
+  memset(&a, 0, sizeof a);
+  a.M = static_cast<int>(d.M);
+  a.N = static_cast<int>(d.N);
+  a.K = static_cast<int>(d.K);
+  a.tiles_m = plan->tiles_m;
+  a.tiles_n = plan->tiles_n;
+  a.out = d.out;
+  a.ldo = d.ldo;
+  a.out_f32 = d.out_f32;
+  a.ldo32 = d.ldo32;
+  a.bias = d.bias;
+  a.mask = d.mask;
+  a.ldm = d.ldm;
+  const int out_elem = (d.epilogue == EPI_F32) ? 4 : 2;
+  a.vec_out = aligned16(d.out, d.ldo, out_elem) ? 1 : 0;
+  a.vec_out32 = aligned16(d.out_f32, d.ldo32, 4) ? 1 : 0;
+  a.vec_mask = aligned16(d.mask, d.ldm, 2) ? 1 : 0;
+  if ((d.epilogue == EPI_F32 && !d.out_f32) || (d.epilogue == EPI_TRUNC16 && !d.out) ||
+      (d.epilogue == EPI_RELUGRAD && (!d.out || !d.mask)) ||
+      (d.epilogue == EPI_BIAS_RELU && (!d.bias || (!d.out && !d.out_f32)))) {
+    snprintf(g_err, sizeof g_err, "missing GEMM epilogue operand (epi=%d)", d.epilogue);
+    return cudaErrorInvalidValue;
+  }
+  int clusters = (num_sms - (d.max_ctas > 0 ? 0 : 0)) / CG;
+  if (d.max_ctas > 0 && d.max_ctas < num_sms) clusters = d.max_ctas / CG;
+  const int tiles = plan->tiles_m * plan->tiles_n;
+  if (clusters > tiles) clusters = tiles;
+  if (clusters < 1) clusters = 1;
+  plan->grid = clusters * CG;
+  return cudaSuccess;
+}
+
+cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t stream) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3(plan.grid, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = plan.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = plan.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[3] = {const_cast<CUtensorMap*>(&plan.tmA), const_cast<CUtensorMap*>(&plan.tmB),
+                   const_cast<GemmArgs*>(&plan.args)};
+  cudaError_t e = cudaLaunchKernelExC(&cfg, plan.kernel, args);
+  if (e != cudaSuccess) snprintf(g_err, sizeof g_err, "GEMM launch failed: %s", cudaGetErrorString(e));
+  return e;
+}
+
+}  // namespace dflow

@@ -1,0 +1,324 @@
+// NK1-NK3: persistent, warp-specialised tcgen05 GEMM for sm_100a with fused
+// epilogues (BiasAdd+Relu, ReluGrad, fp32 store, 32->16 truncation).
+//
+//   C[m, n] = sum_k A(m, k) * B(k, n)        bf16 operands, fp32 accumulate in TMEM
+//
+// Operand majors (what the MLP step needs):
+//   forward  A_{l-1}[b,in]  (K-major)   x  W_l[in,out]      (MN-major B)
+//   dgrad    dZ_l[b,out]    (K-major)   x  W_l as [in,out]  (K-major B: N=in, K=out)
+//   wgrad    A_{l-1}[b,in]  (MN-major)  x  dZ_l[b,out]      (MN-major B)
+//
+// Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA
+// only), warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lane quarters
+// 0..3).  Pipelines: smem stages full/empty (TMA <-> MMA), a double-buffered
+// TMEM accumulator full/empty (MMA <-> epilogue), and a static persistent tile
+// schedule (grid = #SMs / CG clusters, M-grouped tile order for L2 reuse).
+// CG = 2 runs cta_group::2: an MMA of M = 256 spans a CTA pair; each CTA loads
+// half of A (its 128 rows) and half of B (BN/2 columns); completions are
+// signalled on the leader's barriers; commits multicast to both CTAs.
+//
+// Shared-memory tiles use the 128-byte swizzle (1024-byte atoms of 8 x 128 B):
+//   K-major  tile [rows][64 k]            : SBO = 1024 B, k-step of 16 = +32 B
+//   MN-major tile [mn/64][64 k][64 mn]    : LBO = 8192 B (next 64-wide MN chunk),
+//                                           SBO = 1024 B (next 8 k-rows), k-step = +2048 B
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace dflow {
+
+template <int BN, int CG>
+struct GemmCfg {
+  static constexpr int BM = 128;                 // rows per CTA
+  static constexpr int BK = 64;                  // 64 bf16 = one 128-byte swizzle row
+  static constexpr int BN_CTA = BN / CG;         // B columns loaded by each CTA
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN_CTA * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;       // two accumulator buffers
+  static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + alignment slack
+  static_assert(TMEM_COLS >= 32 && TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "tmem cols");
+  static_assert(BN % 32 == 0 && BN_CTA % 64 == 0, "tile N");
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  constexpr int GROUP = 8;
+  const int per_group = GROUP * tiles_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP;
+  const int gsize = min(tiles_m - first_m, GROUP);
+  const int r = t - g * per_group;
+  tm = first_m + r % gsize;
+  tn = r / gsize;
+}
+
+__device__ __forceinline__ float u32_as_f32(uint32_t x) { return __uint_as_float(x); }
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
+__global__ void __launch_bounds__(256, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const GemmArgs args) {
+  using Cfg = GemmCfg<BN, CG>;
+  constexpr int BM = Cfg::BM, BK = Cfg::BK, BN_CTA = Cfg::BN_CTA, STAGES = Cfg::STAGES;
+  constexpr int A_BYTES = Cfg::A_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(tiles + STAGES * STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + STAGES;
+  uint64_t* tfull = bars + 2 * STAGES;
+  uint64_t* tempty = bars + 2 * STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t cta_rank = (CG == 2) ? ptx::cluster_ctarank() : 0;
+  const int cluster_id = blockIdx.x / CG;
+  const int num_clusters = gridDim.x / CG;
+  const int num_tiles = args.tiles_m * args.tiles_n;
+  const int num_kb = (args.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(ptx::smem_u32(&full[s]), 1);
+      ptx::mbar_init(ptx::smem_u32(&empty[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(ptx::smem_u32(&tfull[a]), 1);
+      ptx::mbar_init(ptx::smem_u32(&tempty[a]), 4 * CG);
+    }
+    ptx::fence_mbarrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<CG>(ptx::smem_u32(tmem_slot), Cfg::TMEM_COLS);
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0 && num_kb > 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t full0_local = ptx::smem_u32(&full[0]);
+      const uint32_t full0 = (CG == 2) ? ptx::mapa_shared(full0_local, 0) : full0_local;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        int tm, tn;
+        tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+        const int m0 = tm * (BM * CG) + cta_rank * BM;
+        const int n0 = tn * BN + cta_rank * BN_CTA;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = full0 + stage * 8;
+          if (cta_rank == 0) ptx::mbar_arrive_expect_tx(ptx::smem_u32(&full[stage]), CG * STAGE_BYTES);
+          const uint32_t sa = ptx::smem_u32(tiles + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+          const int k0 = kb * BK;
+#pragma unroll
+          for (int i = 0; i < (A_MN ? BM / 64 : 1); ++i) {
+            const uint32_t dst = sa + i * (64 * BK * 2);
+            const int c0 = A_MN ? (m0 + 64 * i) : k0;
+            const int c1 = A_MN ? k0 : m0;
+            if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, &tmA, fb, c0, c1);
+            else ptx::tma_load_2d(dst, &tmA, fb, c0, c1);
+          }
+#pragma unroll
+          for (int i = 0; i < (B_MN ? BN_CTA / 64 : 1); ++i) {
+            const uint32_t dst = sb + i * (64 * BK * 2);
+            const int c0 = B_MN ? (n0 + 64 * i) : k0;
+            const int c1 = B_MN ? k0 : n0;
+            if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, &tmB, fb, c0, c1);
+            else ptx::tma_load_2d(dst, &tmB, fb, c0, c1);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (one thread of the leader CTA) =====================
+    if (cta_rank == 0 && lane == 0 && num_kb > 0) {
+      constexpr uint32_t idesc = ptx::make_idesc(BM * CG, BN, A_MN, B_MN, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+        ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(tiles + stage * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
+                                        : ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
+            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
+                                        : ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
+            ptx::mma_ss<CG, false>(d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          ptx::mma_commit<CG>(ptx::smem_u32(&empty[stage]), 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit<CG>(ptx::smem_u32(&tfull[acc]), 0x3);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> registers -> global =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const uint32_t tempty_leader =
+        (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0) : ptx::smem_u32(&tempty[0]);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      int tm, tn;
+      tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+      const int gm = tm * (BM * CG) + cta_rank * BM + q * 32 + lane;
+      const bool row_ok = gm < args.M;
+      if (num_kb > 0) {
+        ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
+        ptx::tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        const int gn = tn * BN + c * 32;
+        uint32_t r[32];
+        if (num_kb > 0) {
+          ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+          ptx::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;  // K == 0: the empty sum
+        }
+        if (row_ok && gn < args.N) {
+        const bool full_chunk = gn + 32 <= args.N;
+        if constexpr (EPI == EPI_F32) {
+          float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
+          if (full_chunk && args.vec_out32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<uint4*>(o + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = u32_as_f32(r[j]);
+          }
+        } else if constexpr (EPI == EPI_TRUNC16) {
+          uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+          if (full_chunk && args.vec_out) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 v;
+              v.x = (r[j] >> 16) | (r[j + 1] & 0xFFFF0000u);
+              v.y = (r[j + 2] >> 16) | (r[j + 3] & 0xFFFF0000u);
+              v.z = (r[j + 4] >> 16) | (r[j + 5] & 0xFFFF0000u);
+              v.w = (r[j + 6] >> 16) | (r[j + 7] & 0xFFFF0000u);
+              *reinterpret_cast<uint4*>(o + j) = v;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = static_cast<uint16_t>(r[j] >> 16);
+          }
+        } else if constexpr (EPI == EPI_BIAS_RELU) {
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float bj = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
+            const float z = __fadd_rn(u32_as_f32(r[j]), bj);
+            v[j] = (z < 0.f) ? 0.f : z;  // Relu; NaN propagates (non-finite guard)
+          }
+          if (args.out != nullptr) {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+            if (full_chunk && args.vec_out) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8)
+                *reinterpret_cast<uint4*>(o + j) =
+                    make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                               pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+            } else {
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = __float2bfloat16_rn(v[j]);
+            }
+          }
+          if (args.out_f32 != nullptr) {
+            float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
+            if (full_chunk && args.vec_out32) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+  #pragma unroll
+              for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = v[j];
+            }
+          }
+        } else if constexpr (EPI == EPI_RELUGRAD) {
+          const __nv_bfloat16* mrow = reinterpret_cast<const __nv_bfloat16*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+          if (full_chunk && args.vec_out && args.vec_mask) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j));
+              const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                // bf16 > 0  <=>  sign bit clear and not +0 (and not NaN)
+                const bool pos = (h & 0x8000u) == 0 && h != 0 && h <= 0x7F80u;
+                v[e] = pos ? u32_as_f32(r[j + e]) : 0.f;
+              }
+              *reinterpret_cast<uint4*>(o + j) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                                                            pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (gn + j >= args.N) continue;
+              const float mj = __bfloat162float(mrow[j]);
+              o[j] = __float2bfloat16_rn(mj > 0.f ? u32_as_f32(r[j]) : 0.f);
+            }
+          }
+        }
+        }  // row_ok && gn < N
+        __syncwarp();
+      }
+      if (num_kb > 0) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+          else ptx::mbar_arrive(ptx::smem_u32(&tempty[acc]));
+        }
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<CG>(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+}  // namespace dflow

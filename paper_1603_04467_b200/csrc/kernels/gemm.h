@@ -1,0 +1,63 @@
+// Host-side GEMM launcher interface (NK1-NK3).  See gemm.cuh for the kernel.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace dflow {
+
+enum GemmEpilogue : int {
+  EPI_F32 = 0,        // out_f32[m,n] = acc
+  EPI_TRUNC16 = 1,    // out_u16[m,n] = bits(acc) >> 16              (a4 + a6 fused)
+  EPI_BIAS_RELU = 2,  // a = relu(acc + bias[n]); out_bf16 (RNE) and/or out_f32  (a1)
+  EPI_RELUGRAD = 3,   // out_bf16 = acc * 1[mask_bf16[m,n] > 0]        (a3)
+};
+
+// Kernel arguments (by value, __grid_constant__-style).
+struct GemmArgs {
+  int M, N, K;
+  int tiles_m, tiles_n;   // tiles of (128*CG) x BN
+  void* out;              // bf16 (BIAS_RELU, RELUGRAD) or u16 (TRUNC16)
+  int64_t ldo;
+  float* out_f32;         // fp32 output (F32, optional for BIAS_RELU)
+  int64_t ldo32;
+  const float* bias;      // [N]
+  const void* mask;       // RELUGRAD: the forward activation A_{l-1} (bf16)
+  int64_t ldm;
+  int vec_out;            // 1: 16-byte vector stores are aligned for out
+  int vec_out32;          // 1: 16-byte vector stores are aligned for out_f32
+  int vec_mask;           // 1: 16-byte vector loads are aligned for mask
+};
+
+struct GemmDesc {
+  int64_t M, N, K;
+  const void* A;  int64_t lda; bool a_mn;   // a_mn=0: A(m,k)=A[m*lda+k]; 1: A(m,k)=A[k*lda+m]
+  const void* B;  int64_t ldb; bool b_mn;   // b_mn=0: B(k,n)=B[n*ldb+k]; 1: B(k,n)=B[k*ldb+n]
+  int epilogue;                             // GemmEpilogue
+  void* out;  int64_t ldo;
+  float* out_f32; int64_t ldo32;
+  const float* bias;
+  const void* mask; int64_t ldm;
+  int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair), 3 = 128x256 (1 CTA)
+  int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)
+};
+
+// Prepared launch: tensor maps + args, reusable across calls while buffers stay put.
+struct GemmPlan {
+  CUtensorMap tmA, tmB;
+  GemmDesc d;
+  GemmArgs args;
+  int tile;
+  int grid;
+  int tiles_m, tiles_n;
+  void* kernel;
+  int smem;
+  int cluster;
+};
+
+// Returns cudaSuccess or an error (cudaErrorInvalidValue for unsupported layouts).
+cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan);
+cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t stream);
+const char* gemm_last_error();
+
+}  // namespace dflow

@@ -1,0 +1,892 @@
+// Replicated synchronous train step (§7 :934-941, Fig.7 top) on one GPU
+// per replica: planner, device state, NCCL exchange with the §5.5 codec, executor.
+//
+// Step schedule for rank r (local batch b = B/N, reading A4):
+//   cast x -> A0 (bf16)                                   NK13
+//   l = 1..L:  A_l = relu(A_{l-1} W_l + b_l)              NK1 (tcgen05 GEMM, fused epilogue)
+//   dZ_L, C_r = loss seed(A_L, y)                         NK7
+//   l = L..1:  dZ_{l-1} = (dZ_l W_l^T) . 1[A_{l-1} > 0]   NK2 (l > 1)
+//              dW_l = A_{l-1}^T dZ_l  [-> trunc16]        NK3
+//              db_l = colsum(dZ_l)    [-> trunc16]        NK8
+//              comm stream: alltoall -> owner fold -> allgather (NCCL, NVLink)   NK11
+//              W_l, b_l <- W - lr * expand(g_hat)         NK12
+#include "session.h"
+
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.h"
+#include "kernels/elementwise.h"
+
+namespace dflow {
+
+namespace {
+
+#define CU(expr)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      s->poisoned = true;                                                                \
+      return fail(DFLOW_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    }                                                                                    \
+  } while (0)
+
+#define NC(expr)                                                                          \
+  do {                                                                                    \
+    ncclResult_t r_ = (expr);                                                             \
+    if (r_ != ncclSuccess) {                                                              \
+      s->poisoned = true;                                                                 \
+      return fail(DFLOW_NCCL, "%s failed: %s", #expr, ncclGetErrorString(r_));           \
+    }                                                                                     \
+  } while (0)
+
+#define ST(expr)                        \
+  do {                                  \
+    dflow_status st_ = (expr);          \
+    if (st_ != DFLOW_OK) return st_;    \
+  } while (0)
+
+inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+int find_node(const Graph& g, Op op, const std::vector<int>& inputs, int ta = -1, int tb = -1) {
+  for (size_t i = 0; i < g.nodes.size(); ++i) {
+    const Node& n = g.nodes[i];
+    if (n.op != op || n.inputs != inputs) continue;
+    if (ta >= 0 && (n.transpose_a != ta || n.transpose_b != tb)) continue;
+    return static_cast<int>(i);
+  }
+  return -1;
+}
+
+// --------------------------------------------------------------------- planner
+dflow_status match_graph(dflow_session* s) {
+  const Graph& g = s->g;
+  const int n = static_cast<int>(g.nodes.size());
+  std::vector<char> used(n, 0);
+  int loss = -1;
+  for (int i = 0; i < n; ++i)
+    if (g.nodes[i].op == Op::Loss) {
+      if (loss >= 0) return fail(DFLOW_UNIMPLEMENTED, "planner: more than one Loss node");
+      loss = i;
+    }
+  if (loss < 0) return fail(DFLOW_UNIMPLEMENTED, "planner: the graph has no Loss node");
+  s->cost = loss;
+  s->loss_kind = g.nodes[loss].loss_kind;
+  used[loss] = 1;
+  if (s->loss_kind == DFLOW_LOSS_MSE) {
+    s->y = g.nodes[loss].inputs[1];
+    if (g.nodes[s->y].op != Op::Placeholder || g.nodes[s->y].dtype != DFLOW_F32)
+      return fail(DFLOW_UNIMPLEMENTED, "planner: the MSE target must be an fp32 Placeholder");
+    used[s->y] = 1;
+  }
+  // walk the forward chain back from the loss prediction
+  std::vector<LayerNodes> rev;
+  int cur = g.nodes[loss].inputs[0];
+  for (;;) {
+    LayerNodes ln;
+    const Node& r = g.nodes[cur];
+    if (r.op != Op::Relu) return fail(DFLOW_UNIMPLEMENTED, "planner: '%s' is not a Relu block", r.name.c_str());
+    ln.relu = cur;
+    ln.add = r.inputs[0];
+    const Node& a = g.nodes[ln.add];
+    if (a.op != Op::Add) return fail(DFLOW_UNIMPLEMENTED, "planner: '%s' is not Add(MatMul, bias)", a.name.c_str());
+    ln.mm = a.inputs[0];
+    ln.b = a.inputs[1];
+    const Node& m = g.nodes[ln.mm];
+    const Node& bn = g.nodes[ln.b];
+    if (m.op != Op::MatMul || m.transpose_a || m.transpose_b || bn.op != Op::Variable || bn.shape.size() != 1)
+      return fail(DFLOW_UNIMPLEMENTED, "planner: '%s' is not Add(MatMul(a, W), b)", a.name.c_str());
+    ln.W = m.inputs[1];
+    const Node& Wn = g.nodes[ln.W];
+    if (Wn.op != Op::Variable || Wn.shape.size() != 2)
+      return fail(DFLOW_UNIMPLEMENTED, "planner: '%s' needs a rank-2 Variable weight", m.name.c_str());
+    rev.push_back(ln);
+    const int prev = m.inputs[0];
+    if (g.nodes[prev].op == Op::Placeholder) {
+      s->x = prev;
+      break;
+    }
+    cur = prev;
+  }
+  std::reverse(rev.begin(), rev.end());
+  s->L = static_cast<int>(rev.size());
+  const Node& xn = g.nodes[s->x];
+  if (xn.shape.size() != 2) return fail(DFLOW_UNIMPLEMENTED, "planner: x must be rank 2");
+  s->x_dtype = xn.dtype;
+  used[s->x] = 1;
+  s->layers.assign(s->L, Layer());
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    ly.n = rev[l];
+    ly.in = g.nodes[ly.n.W].shape[0];
+    ly.out = g.nodes[ly.n.W].shape[1];
+    if (g.nodes[ly.n.b].shape[0] != ly.out) return fail(DFLOW_UNIMPLEMENTED, "planner: bias length mismatch");
+    if (l > 0 && ly.in != s->layers[l - 1].out) return fail(DFLOW_UNIMPLEMENTED, "planner: layer widths do not chain");
+    for (int id : {ly.n.W, ly.n.b, ly.n.mm, ly.n.add, ly.n.relu}) {
+      if (used[id]) return fail(DFLOW_UNIMPLEMENTED, "planner: node '%s' is shared between layers", g.nodes[id].name.c_str());
+      used[id] = 1;
+    }
+  }
+  if (xn.shape[1] != s->layers[0].in) return fail(DFLOW_UNIMPLEMENTED, "planner: x width != W1 rows");
+  // gradient graph: LossGrad -> (ReluGrad -> ReduceSum, MatMul^T...) per layer
+  std::vector<int> lg_in = g.nodes[loss].inputs;
+  s->lossgrad = find_node(g, Op::LossGrad, lg_in);
+  if (s->lossgrad >= 0) {
+    if (g.nodes[s->lossgrad].loss_kind != s->loss_kind) return fail(DFLOW_UNIMPLEMENTED, "planner: LossGrad kind");
+    used[s->lossgrad] = 1;
+    int gin = s->lossgrad;
+    for (int l = s->L - 1; l >= 0; --l) {
+      Layer& ly = s->layers[l];
+      const int aprev = (l == 0) ? s->x : s->layers[l - 1].n.relu;
+      ly.n.relugrad = find_node(g, Op::ReluGrad, {gin, ly.n.relu});
+      if (ly.n.relugrad < 0)
+        return fail(DFLOW_UNIMPLEMENTED, "planner: layer %d has no ReluGrad(g, relu) node on the gradient path", l + 1);
+      ly.n.db = find_node(g, Op::ReduceSum, {ly.n.relugrad});
+      ly.n.dW = find_node(g, Op::MatMul, {aprev, ly.n.relugrad}, 1, 0);
+      ly.n.dX = find_node(g, Op::MatMul, {ly.n.relugrad, ly.n.W}, 0, 1);
+      if (ly.n.db < 0 || ly.n.dW < 0)
+        return fail(DFLOW_UNIMPLEMENTED, "planner: layer %d gradient nodes (db, dW) not found", l + 1);
+      for (int id : {ly.n.relugrad, ly.n.db, ly.n.dW}) used[id] = 1;
+      if (ly.n.dX >= 0) used[ly.n.dX] = 1;
+      if (l > 0) {
+        if (ly.n.dX < 0) return fail(DFLOW_UNIMPLEMENTED, "planner: layer %d has no dX node", l + 1);
+        gin = ly.n.dX;
+      }
+    }
+  }
+  // ApplyGradientDescent nodes, through the exchange chain the compression pass inserted
+  const bool xchg = s->opt.world > 1 && s->opt.exchange != DFLOW_EXCHANGE_NONE;
+  int applies = 0;
+  for (int i = 0; i < n; ++i) {
+    const Node& ap = g.nodes[i];
+    if (ap.op != Op::ApplyGradientDescent) continue;
+    int gid = ap.inputs[1];
+    std::vector<int> chain;
+    if (xchg && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+      const int e = gid;
+      if (g.nodes[e].op != Op::Expand16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing Expand16 before apply");
+      const int m = g.nodes[e].inputs[0];
+      if (g.nodes[m].op != Op::CrossReplicaMeanT16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
+      const int t = g.nodes[m].inputs[0];
+      if (g.nodes[t].op != Op::Truncate16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing Truncate16");
+      chain = {e, m, t};
+      gid = g.nodes[t].inputs[0];
+    } else if (xchg) {
+      if (g.nodes[gid].op != Op::CrossReplicaMean) return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
+      chain = {gid};
+      gid = g.nodes[gid].inputs[0];
+    }
+    bool matched = false;
+    for (Layer& ly : s->layers) {
+      if (ap.inputs[0] == ly.n.W && gid == ly.n.dW && ly.n.apply_W < 0) {
+        ly.n.apply_W = i;
+        ly.n.lr_W = ap.lr;
+        matched = true;
+      } else if (ap.inputs[0] == ly.n.b && gid == ly.n.db && ly.n.apply_b < 0) {
+        ly.n.apply_b = i;
+        ly.n.lr_b = ap.lr;
+        matched = true;
+      }
+      if (matched) break;
+    }
+    if (!matched)
+      return fail(DFLOW_UNIMPLEMENTED, "planner: '%s' does not apply its own layer's gradient", ap.name.c_str());
+    used[i] = 1;
+    for (int c : chain) used[c] = 1;
+    ++applies;
+  }
+  s->trainable = applies == 2 * s->L;
+  if (applies != 0 && !s->trainable)
+    return fail(DFLOW_UNIMPLEMENTED, "planner: every W_l and b_l needs exactly one ApplyGradientDescent");
+  for (int i = 0; i < n; ++i)
+    if (!used[i])
+      return fail(DFLOW_UNIMPLEMENTED, "planner: node '%s' (%s) is not part of a fusable MLP train step",
+                  g.nodes[i].name.c_str(), op_name(g.nodes[i].op));
+  return DFLOW_OK;
+}
+
+template <typename T>
+dflow_status dmalloc(dflow_session* s, T** p, size_t elems) {
+  if (elems == 0) elems = 1;
+  void* v = nullptr;
+  cudaError_t e = cudaMalloc(&v, elems * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(DFLOW_OOM, "cudaMalloc(%zu bytes) failed: %s", elems * sizeof(T), cudaGetErrorString(e));
+  }
+  e = cudaMemset(v, 0, elems * sizeof(T));
+  if (e != cudaSuccess) return fail(DFLOW_CUDA, "cudaMemset failed: %s", cudaGetErrorString(e));
+  *p = static_cast<T*>(v);
+  return DFLOW_OK;
+}
+
+dflow_status alloc_state(dflow_session* s) {
+  const int N = s->opt.world;
+  const int64_t cap = s->cap;
+  s->ld_A0 = pad_to(s->layers[0].in, 8);
+  ST(dmalloc(s, &s->A0, cap * s->ld_A0));
+  int64_t ws = 0, max_out = 0;
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    ly.ld_out = pad_to(ly.out, 8);
+    ly.ld_wb = pad_to(ly.out, 8);
+    ST(dmalloc(s, &ly.W32, ly.in * ly.out));
+    ST(dmalloc(s, &ly.Wbf, ly.in * ly.ld_wb));
+    ST(dmalloc(s, &ly.b32, ly.out));
+    if (l + 1 < s->L) ST(dmalloc(s, &ly.A, cap * ly.ld_out));
+    ST(dmalloc(s, &ly.dZ, cap * ly.ld_out));
+    ly.P = ly.in * ly.out + ly.out;
+    ly.Ppad = pad_to(ly.P, 8 * N);
+    ly.shard = ly.Ppad / N;
+    ST(dmalloc(s, &ly.g32, ly.Ppad));
+    if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+      ST(dmalloc(s, &ly.q16, ly.Ppad));
+      uint16_t *r, *o, *gt;
+      ST(dmalloc(s, &r, ly.Ppad));
+      ST(dmalloc(s, &o, ly.shard));
+      ST(dmalloc(s, &gt, ly.Ppad));
+      ly.recv = r; ly.own = o; ly.gath = gt;
+    } else if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_FP32) {
+      float *r, *o, *gt;
+      ST(dmalloc(s, &r, ly.Ppad));
+      ST(dmalloc(s, &o, ly.shard));
+      ST(dmalloc(s, &gt, ly.Ppad));
+      ly.recv = r; ly.own = o; ly.gath = gt;
+    }
+    ws = std::max<int64_t>(ws, static_cast<int64_t>(colsum_rowchunks(cap, ly.out)) * ly.out);
+    max_out = std::max(max_out, ly.out);
+  }
+  s->ld_AL32 = pad_to(s->layers[s->L - 1].out, 4);
+  ST(dmalloc(s, &s->AL32, cap * s->ld_AL32));
+  ST(dmalloc(s, &s->colsum_ws, ws));
+  ST(dmalloc(s, &s->loss_partials, kLossBlocks));
+  ST(dmalloc(s, &s->loss_dev, 4));
+  s->mask_words_cap = (cap * std::max(max_out, s->layers[0].in) + 31) / 32;
+  ST(dmalloc(s, &s->mask_dev, s->mask_words_cap));
+  if (cudaMallocHost(&s->loss_host, 4 * sizeof(float)) != cudaSuccess)
+    return fail(DFLOW_OOM, "cudaMallocHost failed");
+  if (cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(DFLOW_CUDA, "stream creation failed");
+  s->ev_grad.resize(s->L);
+  s->ev_apply.resize(s->L);
+  for (int l = 0; l < s->L; ++l) {
+    cudaEventCreateWithFlags(&s->ev_grad[l], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&s->ev_apply[l], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&s->ev_loss, cudaEventDisableTiming);
+  return DFLOW_OK;
+}
+
+dflow_status gemm_plan(dflow_session* s, const GemmDesc& d, GemmPlan* p) {
+  cudaError_t e = gemm_prepare(d, s->num_sms, p);
+  if (e != cudaSuccess) return fail(DFLOW_CUDA, "GEMM plan: %s", gemm_last_error());
+  return DFLOW_OK;
+}
+
+dflow_status plan_rows(dflow_session* s, int64_t rows) {
+  if (rows == s->planned_rows) return DFLOW_OK;
+  const int max_ctas = (s->opt.world > 1 && s->opt.overlap && s->opt.sm_reserve > 0)
+                           ? std::max(2, s->num_sms - s->opt.sm_reserve)
+                           : 0;
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    const bool last = (l + 1 == s->L);
+    const __nv_bfloat16* Aprev = (l == 0) ? s->A0 : s->layers[l - 1].A;
+    const int64_t ld_prev = (l == 0) ? s->ld_A0 : s->layers[l - 1].ld_out;
+    GemmDesc f{};
+    f.M = rows; f.N = ly.out; f.K = ly.in;
+    f.A = Aprev; f.lda = ld_prev; f.a_mn = false;
+    f.B = ly.Wbf; f.ldb = ly.ld_wb; f.b_mn = true;
+    f.epilogue = EPI_BIAS_RELU;
+    f.out = last ? nullptr : ly.A; f.ldo = ly.ld_out;
+    f.out_f32 = last ? s->AL32 : nullptr; f.ldo32 = s->ld_AL32;
+    f.bias = ly.b32;
+    f.max_ctas = max_ctas;
+    ST(gemm_plan(s, f, &ly.fwd));
+    ly.has_fwd = true;
+    if (l > 0) {
+      const Layer& lp = s->layers[l - 1];
+      GemmDesc d{};
+      d.M = rows; d.N = ly.in; d.K = ly.out;
+      d.A = ly.dZ; d.lda = ly.ld_out; d.a_mn = false;
+      d.B = ly.Wbf; d.ldb = ly.ld_wb; d.b_mn = false;
+      d.epilogue = EPI_RELUGRAD;
+      d.out = lp.dZ; d.ldo = lp.ld_out;
+      d.mask = lp.A; d.ldm = lp.ld_out;
+      d.max_ctas = max_ctas;
+      ST(gemm_plan(s, d, &ly.dgrad));
+      ly.has_dgrad = true;
+    }
+    GemmDesc w{};
+    w.M = ly.in; w.N = ly.out; w.K = rows;
+    w.A = Aprev; w.lda = ld_prev; w.a_mn = true;
+    w.B = ly.dZ; w.ldb = ly.ld_out; w.b_mn = true;
+    w.epilogue = EPI_F32;
+    w.out_f32 = ly.g32; w.ldo32 = ly.out;
+    w.max_ctas = max_ctas;
+    ST(gemm_plan(s, w, &ly.wgrad32));
+    if (s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+      w.epilogue = EPI_TRUNC16;
+      w.out_f32 = nullptr;
+      w.out = ly.q16; w.ldo = ly.out;
+      ST(gemm_plan(s, w, &ly.wgrad16));
+      ly.has_wgrad16 = true;
+    }
+  }
+  s->planned_rows = rows;
+  return DFLOW_OK;
+}
+
+// ------------------------------------------------------------------ timing
+int tbegin(dflow_session* s, int kind, cudaStream_t st) {
+  if (!s->timing) return -1;
+  if (s->event_next + 2 > s->event_pool.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      s->event_pool.push_back(e);
+    }
+  }
+  TimedRange r{kind, s->event_pool[s->event_next], s->event_pool[s->event_next + 1]};
+  s->event_next += 2;
+  cudaEventRecord(r.a, st);
+  s->ranges.push_back(r);
+  return static_cast<int>(s->ranges.size()) - 1;
+}
+
+void tend(dflow_session* s, int idx, cudaStream_t st) {
+  if (idx >= 0) cudaEventRecord(s->ranges[idx].b, st);
+}
+
+dflow_status launch_gemm(dflow_session* s, const GemmPlan& p, cudaStream_t st) {
+  const int t = tbegin(s, 0, st);
+  cudaError_t e = gemm_launch(p, st);
+  tend(s, t, st);
+  if (e != cudaSuccess) {
+    s->poisoned = true;
+    return fail(DFLOW_CUDA, "%s", gemm_last_error());
+  }
+  s->launches++;
+  s->gemm_launches++;
+  return DFLOW_OK;
+}
+
+dflow_status check_launch(dflow_session* s, cudaError_t e, int count, const char* what) {
+  if (e != cudaSuccess) {
+    s->poisoned = true;
+    return fail(DFLOW_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+  }
+  s->launches += count;
+  return DFLOW_OK;
+}
+
+// ------------------------------------------------------------------ feeds
+struct Feeds {
+  const void* x = nullptr;
+  int64_t ldx = 0;
+  const float* y = nullptr;
+  int64_t ldy = 0;
+};
+
+dflow_status resolve_feeds(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                           const int64_t* ld, Feeds* f) {
+  if (n_feeds < 0 || (n_feeds > 0 && (!feeds || !ptrs || !ld))) return fail(DFLOW_INVALID_ARGUMENT, "bad feed arrays");
+  for (int i = 0; i < n_feeds; ++i) {
+    if (feeds[i] < 0 || feeds[i] >= static_cast<int>(s->remap.size()))
+      return fail(DFLOW_INVALID_ARGUMENT, "feed %d is not a node of the session's graph", i);
+    const int sid = s->remap[feeds[i]];
+    if (sid == s->x) {
+      f->x = ptrs[i];
+      f->ldx = ld[i];
+    } else if (sid == s->y && s->y >= 0) {
+      f->y = static_cast<const float*>(ptrs[i]);
+      f->ldy = ld[i];
+    } else {
+      return fail(DFLOW_INVALID_ARGUMENT, "feed '%s' is not the x or y placeholder", s->g.nodes[sid].name.c_str());
+    }
+  }
+  return DFLOW_OK;
+}
+
+dflow_status check_rows(dflow_session* s, int64_t rows) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
+  if (rows <= 0 || rows > s->cap)
+    return fail(DFLOW_INVALID_ARGUMENT, "local_rows %lld outside 1..max_local_rows=%lld", (long long)rows,
+                (long long)s->cap);
+  if (cudaSetDevice(s->opt.device) != cudaSuccess) return fail(DFLOW_CUDA, "cudaSetDevice failed");
+  return plan_rows(s, rows);
+}
+
+// ------------------------------------------------------------------ phases
+dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStream_t st) {
+  if (!f.x) return fail(DFLOW_INVALID_ARGUMENT, "x must be fed");
+  const int64_t in = s->layers[0].in;
+  if (f.ldx < in) return fail(DFLOW_INVALID_ARGUMENT, "ld of x < its width");
+  int t = tbegin(s, 1, st);
+  cudaError_t e = (s->x_dtype == DFLOW_F32)
+                      ? launch_cast_bf16(static_cast<const float*>(f.x), f.ldx, s->A0, s->ld_A0, rows, in, st)
+                      : launch_copy_bf16(static_cast<const __nv_bfloat16*>(f.x), f.ldx, s->A0, s->ld_A0, rows, in,
+                                         st);
+  tend(s, t, st);
+  ST(check_launch(s, e, 1, "input cast"));
+  for (int l = 0; l < s->L; ++l) ST(launch_gemm(s, s->layers[l].fwd, st));
+  s->have_forward = true;
+  s->last_rows = rows;
+  return DFLOW_OK;
+}
+
+dflow_status run_loss(dflow_session* s, const Feeds& f, int64_t rows, cudaStream_t st) {
+  const Layer& last = s->layers[s->L - 1];
+  if (s->loss_kind == DFLOW_LOSS_MSE && !f.y) return fail(DFLOW_INVALID_ARGUMENT, "y must be fed (MSE loss)");
+  if (s->loss_kind == DFLOW_LOSS_MSE && f.ldy < last.out) return fail(DFLOW_INVALID_ARGUMENT, "ld of y < its width");
+  const int t = tbegin(s, 1, st);
+  cudaError_t e = launch_loss_seed(s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1, s->AL32, s->ld_AL32, f.y, f.ldy, rows,
+                                   last.out, last.dZ, last.ld_out, nullptr, 0, s->loss_partials, s->loss_dev, st);
+  tend(s, t, st);
+  return check_launch(s, e, 2, "loss seed");
+}
+
+// Exchange + apply of layer l (comm stream when N > 1).
+dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
+  Layer& ly = s->layers[l];
+  const int N = s->opt.world;
+  const int64_t nW = ly.in * ly.out;
+  cudaStream_t cs = st;
+  const uint16_t* g16 = nullptr;
+  const float* g32 = ly.g32;
+  if (N > 1) {
+    cs = s->comm;
+    CU(cudaEventRecord(s->ev_grad[l], st));
+    CU(cudaStreamWaitEvent(cs, s->ev_grad[l], 0));
+    const int t = tbegin(s, 2, cs);
+    switch (s->opt.exchange) {
+      case DFLOW_EXCHANGE_TRUNC16: {
+        NC(ncclAlltoAll(ly.q16, ly.recv, ly.shard * 2, ncclUint8, s->nccl, cs));
+        ST(check_launch(s, launch_owner_reduce_t16(static_cast<uint16_t*>(ly.recv), ly.shard, N,
+                                                   static_cast<uint16_t*>(ly.own), cs), 1, "owner reduce"));
+        NC(ncclAllGather(ly.own, ly.gath, ly.shard * 2, ncclUint8, s->nccl, cs));
+        g16 = static_cast<const uint16_t*>(ly.gath);
+        g32 = nullptr;
+        break;
+      }
+      case DFLOW_EXCHANGE_FP32: {
+        NC(ncclAlltoAll(ly.g32, ly.recv, ly.shard, ncclFloat32, s->nccl, cs));
+        ST(check_launch(s, launch_owner_reduce_f32(static_cast<float*>(ly.recv), ly.shard, N,
+                                                   static_cast<float*>(ly.own), cs), 1, "owner reduce"));
+        NC(ncclAllGather(ly.own, ly.gath, ly.shard, ncclFloat32, s->nccl, cs));
+        g32 = static_cast<const float*>(ly.gath);
+        break;
+      }
+      case DFLOW_EXCHANGE_FP32_NCCL: {
+        NC(ncclAllReduce(ly.g32, ly.g32, ly.P, ncclFloat32, ncclSum, s->nccl, cs));
+        ST(check_launch(s, launch_scale_f32(ly.g32, ly.P, 1.0f / static_cast<float>(N), cs), 1, "scale"));
+        break;
+      }
+      default:
+        break;  // NONE: local gradient (timing only)
+    }
+    tend(s, t, cs);
+  }
+  const int t = tbegin(s, 1, cs);
+  cudaError_t e = launch_apply_sgd(ly.W32, g32, g16, ly.in, ly.out, ly.Wbf, ly.ld_wb, ly.n.lr_W, cs);
+  if (e == cudaSuccess)
+    e = launch_apply_sgd(ly.b32, g32 ? g32 + nW : nullptr, g16 ? g16 + nW : nullptr, 1, ly.out, nullptr, 0,
+                         ly.n.lr_b, cs);
+  tend(s, t, cs);
+  ST(check_launch(s, e, 2, "apply"));
+  if (N > 1) CU(cudaEventRecord(s->ev_apply[l], cs));
+  return DFLOW_OK;
+}
+
+// mode 0: train (TRUNC16 buckets + exchange + apply); 1: fetch (fp32 grads, no exchange)
+dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int mode) {
+  const bool t16 = mode == 0 && s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16;
+  for (int l = s->L - 1; l >= 0; --l) {
+    Layer& ly = s->layers[l];
+    if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
+    ST(launch_gemm(s, t16 ? ly.wgrad16 : ly.wgrad32, st));
+    const int t = tbegin(s, 1, st);
+    cudaError_t e = launch_colsum_bf16(ly.dZ, ly.ld_out, rows, ly.out, s->colsum_ws, t16 ? nullptr : ly.g32 + ly.in * ly.out,
+                                       t16 ? ly.q16 + ly.in * ly.out : nullptr, st);
+    tend(s, t, st);
+    ST(check_launch(s, e, 2, "bias-gradient column sum"));
+    if (mode == 0) ST(exchange_apply(s, l, st));
+  }
+  if (mode == 0 && s->opt.world > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
+  return DFLOW_OK;
+}
+
+dflow_status finish_timing(dflow_session* s, cudaStream_t st) {
+  if (!s->timing) return DFLOW_OK;
+  CU(cudaStreamSynchronize(st));
+  if (s->comm) CU(cudaStreamSynchronize(s->comm));
+  for (const TimedRange& r : s->ranges) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.kind == 0) s->gemm_ms += ms;
+    else if (r.kind == 1) s->other_ms += ms;
+    else s->exchange_ms += ms;
+  }
+  s->ranges.clear();
+  s->event_next = 0;
+  return DFLOW_OK;
+}
+
+dflow_status read_loss(dflow_session* s, float* loss_out, cudaStream_t st) {
+  if (!loss_out) return DFLOW_OK;
+  if (s->opt.world > 1) {
+    CU(cudaEventRecord(s->ev_loss, st));
+    CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
+    NC(ncclAllReduce(s->loss_dev, s->loss_dev + 1, 1, ncclFloat32, ncclSum, s->nccl, s->comm));
+    CU(cudaMemcpyAsync(s->loss_host, s->loss_dev + 1, sizeof(float), cudaMemcpyDeviceToHost, s->comm));
+    CU(cudaStreamSynchronize(s->comm));
+    *loss_out = s->loss_host[0] / static_cast<float>(s->opt.world);
+  } else {
+    CU(cudaMemcpyAsync(s->loss_host, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    *loss_out = s->loss_host[0];
+  }
+  s->nonfinite = std::isfinite(*loss_out) ? 0 : 1;
+  return DFLOW_OK;
+}
+
+int layer_of_variable(dflow_session* s, int sid, bool* is_bias) {
+  for (int l = 0; l < s->L; ++l) {
+    if (s->layers[l].n.W == sid) { *is_bias = false; return l; }
+    if (s->layers[l].n.b == sid) { *is_bias = true; return l; }
+  }
+  return -1;
+}
+
+}  // namespace
+
+// ===================================================================== API
+dflow_status session_create(const Graph& user, const dflow_options& opt, const uint8_t* nccl_id,
+                            dflow_session** out) {
+  if (!out) return fail(DFLOW_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world)
+    return fail(DFLOW_INVALID_ARGUMENT, "need 0 <= rank < world");
+  if (opt.precision != DFLOW_PRECISION_BF16 && opt.precision != DFLOW_PRECISION_3XTF32)
+    return fail(DFLOW_INVALID_ARGUMENT, "unknown precision");
+  if (opt.precision == DFLOW_PRECISION_3XTF32)
+    return fail(DFLOW_UNIMPLEMENTED, "the 3xTF32 path is not built yet (SURVEY.md §8 NK4-NK6)");
+  if (opt.exchange < DFLOW_EXCHANGE_TRUNC16 || opt.exchange > DFLOW_EXCHANGE_NONE)
+    return fail(DFLOW_INVALID_ARGUMENT, "unknown exchange mode");
+  if (opt.max_local_rows <= 0) return fail(DFLOW_INVALID_ARGUMENT, "max_local_rows must be > 0");
+  if (opt.world > 1 && !nccl_id) return fail(DFLOW_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
+  dflow_session* s = new dflow_session();
+  s->opt = opt;
+  s->cap = opt.max_local_rows;
+  dflow_status st = insert_exchange(user, opt.world, opt.exchange, &s->g, &s->remap);
+  if (st == DFLOW_OK) st = match_graph(s);
+  if (st != DFLOW_OK) {
+    delete s;
+    return st;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    delete s;
+    return fail(DFLOW_CUDA, "no CUDA device available (dflow has no CPU fallback)");
+  }
+  if (opt.device < 0 || opt.device >= ndev || cudaSetDevice(opt.device) != cudaSuccess) {
+    delete s;
+    return fail(DFLOW_INVALID_ARGUMENT, "bad device ordinal %d", opt.device);
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, opt.device);
+  if (prop.major != 10) {
+    delete s;
+    return fail(DFLOW_CUDA, "dflow kernels are built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
+  }
+  s->num_sms = prop.multiProcessorCount;
+  st = alloc_state(s);
+  if (st == DFLOW_OK && opt.world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&s->nccl, opt.world, id, opt.rank);
+    if (r != ncclSuccess) st = fail(DFLOW_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+  }
+  if (st != DFLOW_OK) {
+    session_destroy(s);
+    return st;
+  }
+  *out = s;
+  return DFLOW_OK;
+}
+
+void session_destroy(dflow_session* s) {
+  if (!s) return;
+  cudaSetDevice(s->opt.device);
+  cudaDeviceSynchronize();
+  if (s->nccl) ncclCommDestroy(s->nccl);
+  for (Layer& ly : s->layers) {
+    for (void* p : {(void*)ly.W32, (void*)ly.Wbf, (void*)ly.b32, (void*)ly.A, (void*)ly.dZ, (void*)ly.g32,
+                    (void*)ly.q16, ly.recv, ly.own, ly.gath})
+      if (p) cudaFree(p);
+  }
+  for (void* p : {(void*)s->A0, (void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->colsum_ws,
+                  (void*)s->mask_dev, s->host_stage[0], s->host_stage[1]})
+    if (p) cudaFree(p);
+  if (s->loss_host) cudaFreeHost(s->loss_host);
+  for (cudaEvent_t e : s->ev_grad) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->ev_apply) cudaEventDestroy(e);
+  for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
+  if (s->ev_loss) cudaEventDestroy(s->ev_loss);
+  if (s->comm) cudaStreamDestroy(s->comm);
+  cudaGetLastError();
+  delete s;
+}
+
+dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                                const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st) {
+  if (!s->trainable) return fail(DFLOW_UNIMPLEMENTED, "graph has no ApplyGradientDescent nodes to run");
+  ST(check_rows(s, rows));
+  Feeds f;
+  ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
+  s->launches = s->gemm_launches = 0;
+  ST(run_forward(s, f, rows, st));
+  ST(run_loss(s, f, rows, st));
+  ST(run_backward(s, rows, st, 0));
+  CU(cudaGetLastError());
+  s->last_launches = s->launches;
+  s->last_gemm_launches = s->gemm_launches;
+  ST(read_loss(s, loss_out, st));
+  if (s->timing) {
+    ST(finish_timing(s, st));
+    s->timed_steps++;
+  }
+  return DFLOW_OK;
+}
+
+dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                     const void* const* host_ptrs, const int64_t* ld, int64_t rows,
+                                     float* loss_out, cudaStream_t st) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
+  if (n_feeds < 0 || n_feeds > 2 || (n_feeds > 0 && (!feeds || !host_ptrs || !ld)))
+    return fail(DFLOW_INVALID_ARGUMENT, "bad feed arrays");
+  const void* dptrs[2];
+  for (int i = 0; i < n_feeds; ++i) {
+    const int sid = (feeds[i] >= 0 && feeds[i] < (int)s->remap.size()) ? s->remap[feeds[i]] : -1;
+    if (sid < 0) return fail(DFLOW_INVALID_ARGUMENT, "bad feed node");
+    const size_t esz = (sid == s->x && s->x_dtype == DFLOW_BF16) ? 2 : 4;
+    const size_t bytes = static_cast<size_t>(rows) * ld[i] * esz;
+    if (s->host_stage_bytes[i] < bytes) {
+      if (s->host_stage[i]) cudaFree(s->host_stage[i]);
+      s->host_stage[i] = nullptr;
+      if (cudaMalloc(&s->host_stage[i], bytes) != cudaSuccess) return fail(DFLOW_OOM, "staging buffer");
+      s->host_stage_bytes[i] = bytes;
+    }
+    CU(cudaMemcpyAsync(s->host_stage[i], host_ptrs[i], bytes, cudaMemcpyHostToDevice, st));
+    dptrs[i] = s->host_stage[i];
+  }
+  float loss = 0.f;
+  ST(session_train_step(s, n_feeds, feeds, dptrs, ld, rows, &loss, st));
+  if (loss_out) *loss_out = loss;
+  return DFLOW_OK;
+}
+
+dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                             const int64_t* ld, int64_t rows, dflow_node fetch, void* out, cudaStream_t st) {
+  ST(check_rows(s, rows));
+  Feeds f;
+  ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
+  if (fetch < 0 || fetch >= (int)s->remap.size() || !out) return fail(DFLOW_INVALID_ARGUMENT, "bad fetch");
+  const int sid = s->remap[fetch];
+  ST(run_forward(s, f, rows, st));
+  if (sid == s->cost) {
+    ST(run_loss(s, f, rows, st));
+    CU(cudaMemcpyAsync(out, s->loss_dev, sizeof(float), cudaMemcpyDeviceToDevice, st));
+    return DFLOW_OK;
+  }
+  for (int l = 0; l < s->L; ++l) {
+    if (s->layers[l].n.relu != sid) continue;
+    const Layer& ly = s->layers[l];
+    cudaError_t e = (l + 1 == s->L)
+                        ? launch_copy_f32(s->AL32, s->ld_AL32, rows, ly.out, static_cast<float*>(out), ly.out, st)
+                        : launch_bf16_to_f32(ly.A, ly.ld_out, rows, ly.out, static_cast<float*>(out), st);
+    return check_launch(s, e, 1, "fetch copy");
+  }
+  return fail(DFLOW_UNIMPLEMENTED, "forward fetch must be a Relu node or the cost");
+}
+
+dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                     const void* const* ptrs, const int64_t* ld, int64_t rows, int n,
+                                     const dflow_node* grads, void* const* out, cudaStream_t st) {
+  if (s->lossgrad < 0) return fail(DFLOW_UNIMPLEMENTED, "graph has no gradient nodes");
+  ST(check_rows(s, rows));
+  Feeds f;
+  ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
+  if (n < 0 || (n > 0 && (!grads || !out))) return fail(DFLOW_INVALID_ARGUMENT, "bad fetch arrays");
+  ST(run_forward(s, f, rows, st));
+  ST(run_loss(s, f, rows, st));
+  ST(run_backward(s, rows, st, 1));
+  for (int i = 0; i < n; ++i) {
+    const int sid = (grads[i] >= 0 && grads[i] < (int)s->remap.size()) ? s->remap[grads[i]] : -1;
+    bool done = false;
+    for (int l = 0; l < s->L && !done; ++l) {
+      Layer& ly = s->layers[l];
+      if (sid == ly.n.dW) {
+        CU(cudaMemcpyAsync(out[i], ly.g32, ly.in * ly.out * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        done = true;
+      } else if (sid == ly.n.db) {
+        CU(cudaMemcpyAsync(out[i], ly.g32 + ly.in * ly.out, ly.out * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        done = true;
+      } else if (sid == ly.n.dX && l == 0) {
+        // dx = dZ_1 W_1^T (Fig.5), fp32, written straight by the GEMM epilogue
+        GemmDesc d{};
+        d.M = rows; d.N = ly.in; d.K = ly.out;
+        d.A = ly.dZ; d.lda = ly.ld_out; d.a_mn = false;
+        d.B = ly.Wbf; d.ldb = ly.ld_wb; d.b_mn = false;
+        d.epilogue = EPI_F32;
+        d.out_f32 = static_cast<float*>(out[i]); d.ldo32 = ly.in;
+        GemmPlan p;
+        ST(gemm_plan(s, d, &p));
+        ST(launch_gemm(s, p, st));
+        done = true;
+      }
+    }
+    if (!done) return fail(DFLOW_UNIMPLEMENTED, "fetchable gradients are dW_l, db_l and dx");
+  }
+  return DFLOW_OK;
+}
+
+dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_host) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  if (layer < 1 || layer > s->L || !bits_host) return fail(DFLOW_INVALID_ARGUMENT, "layer must be 1..L");
+  if (!s->have_forward) return fail(DFLOW_NOT_INITIALIZED, "no forward pass has run yet");
+  const Layer& ly = s->layers[layer - 1];
+  const int64_t rows = s->last_rows;
+  const int64_t words = (rows * ly.out + 31) / 32;
+  cudaStream_t st = nullptr;
+  cudaError_t e = (layer == s->L) ? launch_relu_mask_bits_f32(s->AL32, s->ld_AL32, rows, ly.out, s->mask_dev, st)
+                                  : launch_relu_mask_bits(ly.A, ly.ld_out, rows, ly.out, s->mask_dev, st);
+  if (e != cudaSuccess) {
+    s->poisoned = true;
+    return fail(DFLOW_CUDA, "mask kernel: %s", cudaGetErrorString(e));
+  }
+  CU(cudaMemcpy(bits_host, s->mask_dev, words * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return DFLOW_OK;
+}
+
+dflow_status session_variable_assign(dflow_session* s, dflow_node var, const void* src, int on_dev, cudaStream_t st) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  if (var < 0 || var >= (int)s->remap.size() || !src) return fail(DFLOW_INVALID_ARGUMENT, "bad variable");
+  bool is_bias;
+  const int l = layer_of_variable(s, s->remap[var], &is_bias);
+  if (l < 0) return fail(DFLOW_INVALID_ARGUMENT, "node is not a Variable of the planned MLP");
+  cudaSetDevice(s->opt.device);
+  Layer& ly = s->layers[l];
+  float* dst = is_bias ? ly.b32 : ly.W32;
+  const size_t bytes = (is_bias ? ly.out : ly.in * ly.out) * sizeof(float);
+  if (on_dev) {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CU(cudaStreamSynchronize(st));
+    CU(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  }
+  if (!is_bias) {
+    cudaError_t e = launch_cast_bf16(ly.W32, ly.out, ly.Wbf, ly.ld_wb, ly.in, ly.out, st);
+    if (e != cudaSuccess) {
+      s->poisoned = true;
+      return fail(DFLOW_CUDA, "weight cast: %s", cudaGetErrorString(e));
+    }
+  }
+  if (!on_dev) CU(cudaStreamSynchronize(st));
+  return DFLOW_OK;
+}
+
+dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, int on_dev, cudaStream_t st) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  if (var < 0 || var >= (int)s->remap.size() || !dst) return fail(DFLOW_INVALID_ARGUMENT, "bad variable");
+  bool is_bias;
+  const int l = layer_of_variable(s, s->remap[var], &is_bias);
+  if (l < 0) return fail(DFLOW_INVALID_ARGUMENT, "node is not a Variable of the planned MLP");
+  cudaSetDevice(s->opt.device);
+  Layer& ly = s->layers[l];
+  const float* src = is_bias ? ly.b32 : ly.W32;
+  const size_t bytes = (is_bias ? ly.out : ly.in * ly.out) * sizeof(float);
+  if (on_dev) {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  } else {
+    CU(cudaStreamSynchronize(st));
+    CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+  }
+  return DFLOW_OK;
+}
+
+dflow_status session_exchange(dflow_session* s, const float* grad, float* out, size_t n, cudaStream_t st) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  const int N = s->opt.world;
+  cudaSetDevice(s->opt.device);
+  if (N == 1 || s->opt.exchange == DFLOW_EXCHANGE_NONE) {  // no channel, no codec (reading A6)
+    CU(cudaMemcpyAsync(out, grad, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    return DFLOW_OK;
+  }
+  const int64_t npad = pad_to(static_cast<int64_t>(n), 8 * N), shard = npad / N;
+  void *send = nullptr, *recv = nullptr, *own = nullptr, *gath = nullptr;
+  const size_t esz = s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 ? 2 : 4;
+  CU(cudaMalloc(&send, npad * esz));
+  CU(cudaMalloc(&recv, npad * esz));
+  CU(cudaMalloc(&own, shard * esz));
+  CU(cudaMalloc(&gath, npad * esz));
+  CU(cudaMemsetAsync(send, 0, npad * esz, st));
+  cudaError_t e = cudaSuccess;
+  if (s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+    e = launch_truncate16(grad, static_cast<uint16_t*>(send), n, st);
+  } else {
+    e = cudaMemcpyAsync(send, grad, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
+  }
+  CU(e);
+  CU(cudaEventRecord(s->ev_loss, st));
+  CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
+  cudaStream_t cs = s->comm;
+  if (s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+    NC(ncclAlltoAll(send, recv, shard * 2, ncclUint8, s->nccl, cs));
+    CU(launch_owner_reduce_t16(static_cast<uint16_t*>(recv), shard, N, static_cast<uint16_t*>(own), cs));
+    NC(ncclAllGather(own, gath, shard * 2, ncclUint8, s->nccl, cs));
+    CU(launch_expand16(static_cast<uint16_t*>(gath), out, n, cs));
+  } else if (s->opt.exchange == DFLOW_EXCHANGE_FP32) {
+    NC(ncclAlltoAll(send, recv, shard, ncclFloat32, s->nccl, cs));
+    CU(launch_owner_reduce_f32(static_cast<float*>(recv), shard, N, static_cast<float*>(own), cs));
+    NC(ncclAllGather(own, gath, shard, ncclFloat32, s->nccl, cs));
+    CU(cudaMemcpyAsync(out, gath, n * sizeof(float), cudaMemcpyDeviceToDevice, cs));
+  } else {
+    NC(ncclAllReduce(send, gath, npad, ncclFloat32, ncclSum, s->nccl, cs));
+    CU(launch_scale_f32(static_cast<float*>(gath), npad, 1.0f / N, cs));
+    CU(cudaMemcpyAsync(out, gath, n * sizeof(float), cudaMemcpyDeviceToDevice, cs));
+  }
+  CU(cudaStreamSynchronize(cs));
+  cudaFree(send);
+  cudaFree(recv);
+  cudaFree(own);
+  cudaFree(gath);
+  return DFLOW_OK;
+}
+
+dflow_status session_stats(dflow_session* s, dflow_stats* out) {
+  if (!out) return fail(DFLOW_INVALID_ARGUMENT, "out is NULL");
+  memset(out, 0, sizeof *out);
+  out->launches_per_step = s->last_launches;
+  out->gemm_launches_per_step = s->last_gemm_launches;
+  out->layers = s->L;
+  out->nonfinite = s->nonfinite;
+  out->gemm_ms = s->gemm_ms;
+  out->other_ms = s->other_ms;
+  out->exchange_ms = s->exchange_ms;
+  out->timed_steps = s->timed_steps;
+  const int64_t b = s->planned_rows > 0 ? s->planned_rows : 0;
+  double f = 0;
+  for (int l = 0; l < s->L; ++l) {
+    const double io = static_cast<double>(s->layers[l].in) * s->layers[l].out;
+    f += 2.0 * b * io * (l > 0 ? 3 : 2);
+  }
+  out->gemm_flops_per_step = f;
+  return DFLOW_OK;
+}
+
+}  // namespace dflow

@@ -1,0 +1,115 @@
+// Replicated train-step session: planner (graph -> fused kernel schedule),
+// device state, NCCL exchange, and the step executor.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/dflow.h"
+#include "graph.h"
+#include "kernels/gemm.h"
+
+namespace dflow {
+
+// One Relu(A W + b) block of the chain plus its gradient nodes (session-graph ids).
+struct LayerNodes {
+  int W = -1, b = -1, mm = -1, add = -1, relu = -1;
+  int relugrad = -1, db = -1, dW = -1, dX = -1;
+  int apply_W = -1, apply_b = -1;
+  float lr_W = 0.f, lr_b = 0.f;
+};
+
+struct Layer {
+  LayerNodes n;
+  int64_t in = 0, out = 0;
+  int64_t ld_out = 0;             // padded leading dim (elements) of bf16 [rows, out] buffers
+  int64_t ld_wb = 0;              // padded leading dim of the bf16 weight copy [in, ld_wb]
+  float* W32 = nullptr;           // fp32 master [in*out] dense
+  __nv_bfloat16* Wbf = nullptr;   // bf16 working copy [in, ld_wb]
+  float* b32 = nullptr;           // fp32 [out]
+  __nv_bfloat16* A = nullptr;     // bf16 activation [cap, ld_out] (all layers; last for masks)
+  __nv_bfloat16* dZ = nullptr;    // bf16 [cap, ld_out]
+  // gradient bucket [dW_l || db_l], padded to Ppad = roundup(P, 8N)
+  int64_t P = 0, Ppad = 0, shard = 0;
+  float* g32 = nullptr;           // fp32 gradient bucket [Ppad]
+  uint16_t* q16 = nullptr;        // TRUNC16 send bucket [Ppad]
+  void* recv = nullptr;           // alltoall landing [Ppad] (u16 or f32)
+  void* own = nullptr;            // owner's reduced shard [shard]
+  void* gath = nullptr;           // allgather landing [Ppad]
+  GemmPlan fwd, dgrad, wgrad32, wgrad16;
+  bool has_fwd = false, has_dgrad = false, has_wgrad16 = false;
+};
+
+struct TimedRange {
+  int kind;  // 0 gemm, 1 other, 2 exchange
+  cudaEvent_t a, b;
+};
+
+}  // namespace dflow
+
+struct dflow_session {
+  dflow::Graph g;                 // rewritten (replicated + compression) graph
+  std::vector<int> remap;         // user graph id -> session graph id
+  dflow_options opt{};
+  int L = 0;
+  std::vector<dflow::Layer> layers;
+  int x = -1, y = -1, cost = -1, lossgrad = -1, loss_kind = 0;
+  dflow_dtype x_dtype = DFLOW_F32;
+  bool trainable = false;
+  int64_t cap = 0;
+  int num_sms = 148;
+  int64_t planned_rows = -1;
+  __nv_bfloat16* A0 = nullptr;    // bf16 copy of the x feed [cap, ld_A0]
+  int64_t ld_A0 = 0;
+  float* AL32 = nullptr;          // fp32 last activation [cap, ld_AL32]
+  int64_t ld_AL32 = 0;
+  double* loss_partials = nullptr;
+  float* loss_dev = nullptr;      // [2]: local C_r, reduced sum
+  float* loss_host = nullptr;     // pinned
+  float* colsum_ws = nullptr;
+  uint32_t* mask_dev = nullptr;
+  int64_t mask_words_cap = 0;
+  void* host_stage[2] = {nullptr, nullptr};  // device copies of host feeds (e2e path)
+  size_t host_stage_bytes[2] = {0, 0};
+  cudaStream_t comm = nullptr;
+  std::vector<cudaEvent_t> ev_grad, ev_apply;
+  cudaEvent_t ev_loss = nullptr;
+  ncclComm_t nccl = nullptr;
+  bool poisoned = false;
+  bool have_forward = false;
+  int64_t last_rows = 0;
+  // timing / stats
+  bool timing = false;
+  std::vector<dflow::TimedRange> ranges;
+  std::vector<cudaEvent_t> event_pool;
+  size_t event_next = 0;
+  double gemm_ms = 0, other_ms = 0, exchange_ms = 0;
+  int64_t timed_steps = 0;
+  int launches = 0, gemm_launches = 0;
+  int last_launches = 0, last_gemm_launches = 0;
+  int nonfinite = 0;
+};
+
+namespace dflow {
+dflow_status session_create(const Graph& user, const dflow_options& opt, const uint8_t* nccl_id,
+                            dflow_session** out);
+void session_destroy(dflow_session* s);
+dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                                const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st);
+dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                     const void* const* host_ptrs, const int64_t* ld, int64_t rows,
+                                     float* loss_out, cudaStream_t st);
+dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                             const int64_t* ld, int64_t rows, dflow_node fetch, void* out, cudaStream_t st);
+dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                     const void* const* ptrs, const int64_t* ld, int64_t rows, int n,
+                                     const dflow_node* grads, void* const* out, cudaStream_t st);
+dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_host);
+dflow_status session_variable_assign(dflow_session* s, dflow_node var, const void* src, int on_dev, cudaStream_t st);
+dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, int on_dev, cudaStream_t st);
+dflow_status session_exchange(dflow_session* s, const float* grad, float* out, size_t n, cudaStream_t st);
+dflow_status session_stats(dflow_session* s, dflow_stats* out);
+}  // namespace dflow

@@ -1,0 +1,135 @@
+"""Test-side harness: drives libdflow through its C ABI with torch CUDA tensors.
+
+Only marshalling; no arithmetic of the method.  Used by the -m gpu tests.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+import paper_1603_04467_b200 as D
+
+
+def dev_ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def stream_ptr():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Run:
+    """One session on one GPU holding an MLP graph."""
+
+    def __init__(self, dims, loss="MSE", lr=0.25, rows=256, exchange="TRUNC16", world=1, rank=0, device=0,
+                 with_dx=False, nccl_id=None, overlap=1, sm_reserve=0, train=True):
+        self.mlp = D.mlp_graph(dims, loss, lr, with_dx=with_dx, train=train)
+        self.dims = tuple(dims)
+        self.loss = loss
+        opts = D.make_options(world=world, rank=rank, device=device, exchange=exchange, max_local_rows=rows,
+                              overlap=overlap, sm_reserve=sm_reserve)
+        self.s = D.session_create(self.mlp, opts, nccl_id)
+
+    def close(self):
+        if self.s:
+            D.dflow_session_destroy(self.s)
+            self.s = None
+        if self.mlp.graph:
+            D.dflow_graph_destroy(self.mlp.graph)
+            self.mlp.graph = None
+
+    def assign(self, Ws, bs):
+        for nid, W in zip(self.mlp.weights, Ws):
+            a = np.ascontiguousarray(W, np.float32)
+            D.check(D.dflow_variable_assign(self.s, nid, a.ctypes.data_as(C.c_void_p), 0, stream_ptr()))
+        for nid, b in zip(self.mlp.biases, bs):
+            a = np.ascontiguousarray(b, np.float32)
+            D.check(D.dflow_variable_assign(self.s, nid, a.ctypes.data_as(C.c_void_p), 0, stream_ptr()))
+
+    def read(self):
+        Ws, bs = [], []
+        for l, nid in enumerate(self.mlp.weights):
+            a = np.empty((self.dims[l], self.dims[l + 1]), np.float32)
+            D.check(D.dflow_variable_read(self.s, nid, a.ctypes.data_as(C.c_void_p), 0, stream_ptr()))
+            Ws.append(a)
+        for l, nid in enumerate(self.mlp.biases):
+            a = np.empty((self.dims[l + 1],), np.float32)
+            D.check(D.dflow_variable_read(self.s, nid, a.ctypes.data_as(C.c_void_p), 0, stream_ptr()))
+            bs.append(a)
+        return Ws, bs
+
+    def _feeds(self, X: torch.Tensor, Y):
+        ids, ptrs, lds = [self.mlp.x], [X.data_ptr()], [X.stride(0)]
+        if Y is not None:
+            ids.append(self.mlp.y)
+            ptrs.append(Y.data_ptr())
+            lds.append(Y.stride(0))
+        return D.node_array(ids), D.ptr_array(ptrs), D.i64_array(lds), len(ids)
+
+    def step(self, X: torch.Tensor, Y=None, want_loss=True):
+        ids, ptrs, lds, n = self._feeds(X, Y)
+        loss = C.c_float(0)
+        D.check(D.dflow_train_step(self.s, n, ids, ptrs, lds, X.shape[0], C.byref(loss) if want_loss else None,
+                                   stream_ptr()))
+        return loss.value
+
+    def gradients(self, X: torch.Tensor, Y=None, with_dx=False):
+        ids, ptrs, lds, n = self._feeds(X, Y)
+        outs, nodes = [], []
+        for l in range(len(self.dims) - 1):
+            outs.append(torch.empty((self.dims[l], self.dims[l + 1]), dtype=torch.float32, device=X.device))
+            nodes.append(self.mlp.grads[self.mlp.weights[l]])
+            outs.append(torch.empty((self.dims[l + 1],), dtype=torch.float32, device=X.device))
+            nodes.append(self.mlp.grads[self.mlp.biases[l]])
+        if with_dx:
+            outs.append(torch.empty((X.shape[0], self.dims[0]), dtype=torch.float32, device=X.device))
+            nodes.append(self.mlp.dx)
+        D.check(D.dflow_fetch_gradients(self.s, n, ids, ptrs, lds, X.shape[0], len(nodes), D.node_array(nodes),
+                                        D.ptr_array([o.data_ptr() for o in outs]), stream_ptr()))
+        torch.cuda.synchronize()
+        res = [o.cpu().numpy() for o in outs]
+        L = len(self.dims) - 1
+        gW = [res[2 * l] for l in range(L)]
+        gb = [res[2 * l + 1] for l in range(L)]
+        return gW, gb, (res[-1] if with_dx else None)
+
+    def masks(self, rows):
+        """GPU relu masks {relu node name (oracle naming): bool [rows, out]} of the last forward."""
+        out = {}
+        L = len(self.dims) - 1
+        for l in range(1, L + 1):
+            cols = self.dims[l]
+            words = (rows * cols + 31) // 32
+            buf = np.zeros(words, np.uint32)
+            D.check(D.dflow_fetch_relu_masks(self.s, l, buf.ctypes.data_as(C.POINTER(C.c_uint32))))
+            bits = np.unpackbits(buf.view(np.uint8), bitorder="little")[: rows * cols].reshape(rows, cols)
+            name = "ReLU" if L == 1 else f"layer{l}/Relu"
+            out[name] = bits.astype(bool)
+        return out
+
+    def forward(self, X: torch.Tensor, Y=None, fetch=None):
+        ids, ptrs, lds, n = self._feeds(X, Y)
+        if fetch is None:
+            fetch = self.mlp.cost
+        if fetch == self.mlp.cost:
+            out = torch.empty(1, dtype=torch.float32, device=X.device)
+        else:
+            l = self.mlp.relus.index(fetch)
+            out = torch.empty((X.shape[0], self.dims[l + 1]), dtype=torch.float32, device=X.device)
+        D.check(D.dflow_forward(self.s, n, ids, ptrs, lds, X.shape[0], fetch, C.c_void_p(out.data_ptr()),
+                                stream_ptr()))
+        torch.cuda.synchronize()
+        return out.cpu().numpy()
+
+    def stats(self):
+        st = D.dflow_stats()
+        D.check(D.dflow_session_stats(self.s, C.byref(st)))
+        return st
+
+
+def normwise(a, ref):
+    a, ref = np.asarray(a, np.float64), np.asarray(ref, np.float64)
+    den = np.max(np.abs(ref))
+    return float(np.max(np.abs(a - ref)) / den) if den > 0 else float(np.max(np.abs(a)))

@@ -1,0 +1,169 @@
+"""GPU parity of the whole train step vs the oracle (single GPU, N = 1).
+
+Tolerances from north_star: bf16 path within 2e-2 (normwise max relative error
+of W after one step, reading A15 (i)); gradients checked mask-locked at the same
+tolerance (A15 (ii), A22).  P12: bitwise in the exact-arithmetic regime.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.mlp import build_mlp, forward, train_step  # noqa: E402
+from synth import C1, C1_BIAS, C2, C3, batch, exact_regime, init_params, with_batch  # noqa: E402
+from dflow_harness import Run, normwise  # noqa: E402
+
+BF16_TOL = 2e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no CPU fallback)"
+
+
+def _dev(a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _one_step_parity(w, rows=None):
+    rows = rows or w.batch
+    Ws, bs = init_params(w)
+    X, Y = batch(w, rows=rows)
+    run = Run(w.dims, w.loss, w.lr, rows=rows, with_dx=(w.layers == 1))
+    try:
+        run.assign(Ws, bs)
+        Xd, Yd = _dev(X), _dev(Y)
+        # gradients (no update) + the GPU's relu masks for the mask-locked oracle
+        gW, gb, dx = run.gradients(Xd, Yd, with_dx=(w.layers == 1))
+        masks = run.masks(rows)
+        mg = build_mlp(w.dims, w.loss, w.lr, with_dx=(w.layers == 1))
+        locked = train_step(mg, Ws, bs, X, Y, 1, "TRUNC16", masks=[masks])
+        errs = {}
+        for l in range(w.layers):
+            errs[f"dW{l + 1}"] = normwise(gW[l], locked["ghat"][mg.weights[l]])
+            errs[f"db{l + 1}"] = normwise(gb[l], locked["ghat"][mg.biases[l]])
+        if dx is not None:
+            errs["dx"] = normwise(dx, locked["per_replica"][0]["dx"])
+        # one train step; W after vs the (unlocked) oracle — the gate as stated (A15 (i))
+        loss = run.step(Xd, Yd)
+        Wg, bg = run.read()
+        ref = train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+        for l in range(w.layers):
+            errs[f"W{l + 1}_after"] = normwise(Wg[l], ref["W"][l])
+            errs[f"b{l + 1}_after"] = normwise(bg[l], ref["b"][l])
+        errs["loss"] = abs(loss - ref["loss"]) / abs(ref["loss"])
+        return errs, locked["flips"]
+    finally:
+        run.close()
+
+
+@pytest.mark.parametrize("w", [C1, C1_BIAS], ids=["C1", "C1_bias"])
+def test_config1_fig1_step_and_fig5_gradients(w):
+    errs, flips = _one_step_parity(w)
+    print(errs, flips)
+    assert max(errs.values()) < BF16_TOL, errs
+
+
+def test_config2_mnist_step():
+    errs, flips = _one_step_parity(C2)
+    print(errs, flips)
+    assert max(errs.values()) < BF16_TOL, errs
+
+
+@pytest.mark.parametrize("rows", [1, 100, 129, 300])
+def test_ragged_batches(rows):
+    errs, _ = _one_step_parity(with_batch(C2, rows), rows=rows)
+    assert max(errs.values()) < BF16_TOL, errs
+
+
+def test_config3_width_reduced_batch():
+    errs, flips = _one_step_parity(with_batch(C3, 512))
+    print(errs, flips)
+    assert max(errs.values()) < BF16_TOL, errs
+
+
+def test_p12_exact_regime_bitwise():
+    # Every stored intermediate is exact in bf16 and fp32 sums are order-free:
+    # the GPU step must equal the oracle bit for bit (W, b after the step and grads).
+    X, Y, Ws, bs, lr = exact_regime()
+    dims = (784, 1024, 1024, 16)
+    run = Run(dims, "MSE", lr, rows=X.shape[0])
+    try:
+        run.assign(Ws, bs)
+        Xd, Yd = _dev(X), _dev(Y)
+        gW, gb, _ = run.gradients(Xd, Yd)
+        mg = build_mlp(dims, "MSE", lr)
+        ref = train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+        for l in range(3):
+            assert np.array_equal(gW[l], ref["ghat"][mg.weights[l]]), f"dW{l + 1}"
+            assert np.array_equal(gb[l], ref["ghat"][mg.biases[l]]), f"db{l + 1}"
+        loss = run.step(Xd, Yd)
+        Wg, bg = run.read()
+        for l in range(3):
+            assert np.array_equal(Wg[l], ref["W"][l]), f"W{l + 1}"
+            assert np.array_equal(bg[l], ref["b"][l]), f"b{l + 1}"
+        assert loss == pytest.approx(ref["loss"], rel=1e-6)
+    finally:
+        run.close()
+
+
+def test_p9_zero_lr_keeps_weights_bitwise():
+    w = with_batch(C2, 128)
+    Ws, bs = init_params(w)
+    X, Y = batch(w)
+    run = Run(w.dims, "MSE", 0.0, rows=128)
+    try:
+        run.assign(Ws, bs)
+        loss = run.step(_dev(X), _dev(Y))
+        Wg, bg = run.read()
+        for a, b in zip(Wg + bg, Ws + bs):
+            assert np.array_equal(a, b)
+        mg = build_mlp(w.dims, "MSE", 0.0)
+        ref = float(forward(mg, Ws, bs, X, Y)[mg.cost])
+        assert abs(loss - ref) / ref < BF16_TOL
+    finally:
+        run.close()
+
+
+def test_forward_fetch_matches_oracle():
+    w = with_batch(C2, 256)
+    Ws, bs = init_params(w)
+    X, Y = batch(w)
+    run = Run(w.dims, "MSE", w.lr, rows=256)
+    try:
+        run.assign(Ws, bs)
+        Xd, Yd = _dev(X), _dev(Y)
+        a3 = run.forward(Xd, Yd, fetch=run.mlp.relus[-1])
+        c = run.forward(Xd, Yd)
+        mg = build_mlp(w.dims, "MSE", w.lr)
+        ref = forward(mg, Ws, bs, X, Y, fetch=[mg.acts[-1], mg.cost])
+        assert normwise(a3, ref[mg.acts[-1]]) < BF16_TOL
+        assert abs(float(c[0]) - float(ref[mg.cost])) / float(ref[mg.cost]) < BF16_TOL
+    finally:
+        run.close()
+
+
+def test_p16_hundred_steps_config2():
+    # PAPER.md:877-878 lessons 3-4; W after 100 steps within the bf16 tolerance.
+    w = C2
+    Ws, bs = init_params(w)
+    run = Run(w.dims, "MSE", w.lr, rows=w.batch)
+    mg = build_mlp(w.dims, "MSE", w.lr)
+    try:
+        run.assign(Ws, bs)
+        Wr, br = Ws, bs
+        losses_g, losses_r = [], []
+        for step in range(100):
+            X, Y = batch(w, step=step)
+            losses_g.append(run.step(_dev(X), _dev(Y)))
+            ref = train_step(mg, Wr, br, X, Y, 1, "TRUNC16")
+            Wr, br = ref["W"], ref["b"]
+            losses_r.append(ref["loss"])
+        Wg, bg = run.read()
+        errs = [normwise(a, b) for a, b in zip(Wg + bg, Wr + br)]
+        print("loss gpu", losses_g[::10], "oracle", losses_r[::10], "W err", errs)
+        assert max(errs) < BF16_TOL
+        assert losses_g[-1] < losses_g[0]
+    finally:
+        run.close()
