@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""bench.py — replicated Relu(XW+b) MLP train step on B200 (arXiv 1603.04467 §7 sync data parallelism).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--exchange TRUNC16] [--impl reference]
+
+One JSON line on rank 0 (the driver's contract).  Workload: BASELINE.json
+configs[2] = "Wide MLP 4 layers of 8192x8192 bf16, global batch 32768, sync
+data-parallel at 1/2/4/8 B200" (the metric's own config; it fits one GPU).
+N > 1: launched by torchrun, one rank per GPU; the global batch is fixed
+(strong scaling), each rank trains on rows [r*b, (r+1)*b), b = 32768/N, and
+the gradients cross NVLink through NCCL alltoall/allgather of 16-bit truncated
+payloads (§5.5).
+
+`--impl reference` times the oracle (the plain CPU implementation written from
+the paper, oracle/) on this box's host cores on a bounded sample of the same
+workload — the reference arm for this tier.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MLP train-step examples/sec at 1/2/4/8 B200; % tensor-core peak"
+UNIT = "examples/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16_burst": d.get("bf16_tflops", 1590.0), "bf16_sustained": d.get("bf16_tflops_sustained", 1400.0),
+                "hbm": d.get("hbm_gbs", 6650.0), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16_burst": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.device = device
+        self.p = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), float(parts[3]), parts[5:9]))
+            except ValueError:
+                continue
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        maxmhz = max(r[1] for r in rows)
+        load = [r for r in rows if r[2] > 300] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": maxmhz, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(r[2] for r in rows)}
+
+
+# ---------------------------------------------------------------- oracle (CPU) legs
+def oracle_sample(w: synth.Workload, target_s: float, n_steps: int = 1):
+    """Times the oracle (as it stands) on a bounded row sample of workload w."""
+    from oracle.mlp import build_mlp, train_step
+    Ws, bs = synth.init_params(w)
+    mg = build_mlp(w.dims, w.loss, w.lr)
+    rows = 16
+    X, Y = synth.batch(w, rows=rows)
+    t0 = time.perf_counter()
+    train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+    t_probe = time.perf_counter() - t0
+    per_row = t_probe / rows
+    rows = int(max(16, min(w.batch, target_s / max(per_row, 1e-9))))
+    rows = max(16, rows // 16 * 16)
+    X, Y = synth.batch(w, rows=rows)
+    times = []
+    for _ in range(n_steps):
+        t0 = time.perf_counter()
+        train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+        times.append(time.perf_counter() - t0)
+    return rows, times
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args, w):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    # each step: one oracle step on a row sample, sized so W + K steps finish in a few minutes
+    per_step_budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    rows, _ = oracle_sample(w, per_step_budget, n_steps=0)
+    from oracle.mlp import build_mlp, train_step
+    Ws, bs = synth.init_params(w)
+    mg = build_mlp(w.dims, w.loss, w.lr)
+    X, Y = synth.batch(w, rows=rows)
+    for _ in range(args.warmup):
+        train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+    dt = time.perf_counter() - t0
+    value = rows * args.steps / dt
+    sample = f"one oracle (f64 numpy graph executor) step of {w.name} on {rows} rows per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1000 / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, synth/)",
+            "config": config_dict(w, args, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(w, args, world):
+    return {"workload": w.name, "global_batch": w.batch, "layers": w.layers, "width": w.dims[1],
+            "dims": list(w.dims), "loss": w.loss, "lr": w.lr, "exchange": args.exchange,
+            "parallelism": f"dp{world}", "precision": "bf16 operands, fp32 accumulate + master weights",
+            "l2": "no flush: every step streams inputs and activations far larger than the 126 MB L2 "
+                  "(X fp32 1 GiB, each activation 512 MiB at N=1)"}
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_gpu(args, w):
+    import torch
+    rank, world, local = env_rank()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1603_04467_b200 as D
+
+    if w.batch % world:
+        raise SystemExit("global batch must divide by the number of GPUs")
+    b = w.batch // world
+    # NCCL id from rank 0, broadcast through torch.distributed (plumbing only)
+    nid = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid = bytes(idt.cpu().numpy().tobytes())
+    mlp = D.mlp_graph(w.dims, w.loss, w.lr)
+    opts = D.make_options(world=world, rank=rank, device=local, exchange=args.exchange, max_local_rows=b,
+                          overlap=1, sm_reserve=args.sm_reserve)
+    s = D.session_create(mlp, opts, nid)
+    Ws, bs = synth.init_params(w)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    for nid_, W in zip(mlp.weights, Ws):
+        D.check(D.dflow_variable_assign(s, nid_, W.ctypes.data_as(C.c_void_p), 0, sp))
+    for nid_, bb in zip(mlp.biases, bs):
+        D.check(D.dflow_variable_assign(s, nid_, bb.ctypes.data_as(C.c_void_p), 0, sp))
+    del Ws, bs
+    X, Y = synth.batch(w, rows=b, row0=rank * b)
+    Xd = torch.from_numpy(X).cuda()
+    Yd = torch.from_numpy(Y).cuda()
+    feeds = D.node_array([mlp.x, mlp.y])
+    ptrs = D.ptr_array([Xd.data_ptr(), Yd.data_ptr()])
+    lds = D.i64_array([Xd.stride(0), Yd.stride(0)])
+
+    def step(loss=None):
+        D.check(D.dflow_train_step(s, 2, feeds, ptrs, lds, b, loss, sp))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    first_loss = C.c_float(0)
+    step(C.byref(first_loss))
+    for _ in range(max(0, args.warmup - 1)):
+        step()
+    clocks = Clocks(local)
+    barrier()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    st = D.dflow_stats()
+    D.check(D.dflow_session_stats(s, C.byref(st)))
+    launches = st.launches_per_step
+    # per-kernel timing pass (CUDA events around every launch on its own stream)
+    D.check(D.dflow_session_set_timing(s, 1))
+    tsteps = max(3, min(args.steps, 10))
+    for _ in range(tsteps):
+        step()
+    D.check(D.dflow_session_stats(s, C.byref(st)))
+    D.check(D.dflow_session_set_timing(s, 0))
+    gemm_avg_ms = st.gemm_ms / max(1, st.timed_steps * st.gemm_launches_per_step)
+    flops_per_launch = st.gemm_flops_per_step / max(1, st.gemm_launches_per_step)
+    last_loss = C.c_float(0)
+    step(C.byref(last_loss))
+
+    # end-to-end through the public API with HOST buffers (pinned), copies inside the timed region
+    Xh = torch.from_numpy(X).pin_memory()
+    Yh = torch.from_numpy(Y).pin_memory()
+    hptrs = D.ptr_array([Xh.data_ptr(), Yh.data_ptr()])
+    hl = C.c_float(0)
+    D.check(D.dflow_train_step_host(s, 2, feeds, hptrs, lds, b, C.byref(hl), sp))
+    e2e_steps = max(3, min(args.steps, 5))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        D.check(D.dflow_train_step_host(s, 2, feeds, hptrs, lds, b, C.byref(hl), sp))
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+
+    pk = peaks()
+    step_flops = w.flops_per_example() * w.batch
+    value = w.batch * args.steps / (ms / 1000.0)
+    achieved = flops_per_launch / (gemm_avg_ms / 1000.0) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(w.name)
+        except Exception:
+            traffic = None
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rows, times = oracle_sample(w, args.cpu_seconds)
+            cpu = {"value": rows / times[0], "unit": UNIT, "cores": cores(), "kind": "oracle",
+                   "sample": f"one oracle (f64 numpy graph executor) train step of {w.name} on a {rows}-row "
+                             f"sample of the global batch ({times[0]:.1f} s)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded, synth/; X,Y ~ U[0,1), He-uniform W)",
+            "config": config_dict(w, args, world),
+            "pct_tensor_peak": {"step_tflops": step_flops / (ms / args.steps / 1000.0) / 1e12 / world,
+                                "per_gpu_frac_of_sustained": step_flops / (ms / args.steps / 1000.0) / 1e12 / world
+                                / pk["bf16_sustained"],
+                                "per_gpu_frac_of_burst": step_flops / (ms / args.steps / 1000.0) / 1e12 / world
+                                / pk["bf16_burst"]},
+            "roofline": {"kernel": "gemm_bf16_kernel (tcgen05 NK1-NK3)", "bound": "tensor", "achieved": achieved,
+                         "peak": pk["bf16_sustained"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sustained"],
+                         "traffic": traffic, "peak_source": pk["source"] + ", sustained bf16 (kernel timed inside "
+                                                                            "a long step)",
+                         "avg_launch_ms": gemm_avg_ms, "flops_per_launch": flops_per_launch,
+                         "gemm_share_of_step": st.gemm_ms / max(1e-9, st.gemm_ms + st.other_ms + st.exchange_ms)},
+            "cpu_baseline": cpu,
+            "e2e": {"value": w.batch * e2e_steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": int(X.nbytes + Y.nbytes) * world, "d2h_bytes_per_step": 4 * world},
+            "gpu_launches": launches * args.steps,
+            "clocks": clk,
+            "loss": {"first": first_loss.value, "last": last_loss.value},
+        }
+        print(json.dumps(line), flush=True)
+    D.dflow_session_destroy(s)
+    D.dflow_graph_destroy(mlp.graph)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dflow", choices=["dflow", "reference"])
+    ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--batch", type=int, default=0, help="override the global batch (parity/debug only)")
+    ap.add_argument("--exchange", default="TRUNC16", choices=["TRUNC16", "FP32", "FP32_NCCL", "NONE"])
+    ap.add_argument("--sm-reserve", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("timing rules: --warmup must be >= 3")
+    w = synth.CONFIGS[args.config]
+    if args.batch:
+        w = synth.with_batch(w, args.batch)
+    if args.impl == "reference":
+        return run_reference(args, w)
+    return run_gpu(args, w)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
