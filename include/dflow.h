@@ -102,6 +102,14 @@ dflow_status dflow_apply_gradient_descent(dflow_graph* g, const char* name, dflo
  * DFLOW_BUFFER_TOO_SMALL if cap < *needed. */
 dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, size_t* needed);
 
+/* Compression-insertion pass alone (host only): *out = a new graph equal to g with,
+ * for world > 1, Truncate16 -> CrossReplicaMeanT16 -> Expand16 (TRUNC16) or
+ * CrossReplicaMean (FP32 modes) between every gradient and its ApplyGradientDescent
+ * (PAPER.md:813-821 on the :934-941 channel).  world == 1 / NONE: a copy (reading A6).
+ * The caller owns *out (dflow_graph_destroy).  Node ids of g keep their meaning for
+ * every node of g in *out only through dflow_node_by_name.                       */
+dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int exchange, dflow_graph** out);
+
 /* ---------------------------------------------------------------- session
  * One session per (rank, GPU).  dflow_session_create copies the graph (an
  * immutable snapshot), runs the replication + compression-insertion pass and

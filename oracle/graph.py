@@ -33,7 +33,9 @@ NON_SCALAR_TARGET = "NON_SCALAR_TARGET"
 INVALID_ARGUMENT = "INVALID_ARGUMENT"
 
 OPS = ("Placeholder", "Variable", "MatMul", "Add", "Relu", "Loss", "LossGrad", "ReluGrad",
-       "ReduceSum", "AddN", "ZerosLike", "ApplyGradientDescent")
+       "ReduceSum", "AddN", "ZerosLike", "ApplyGradientDescent",
+       # inserted by insert_exchange (the replicated graph's transfer nodes)
+       "Truncate16", "CrossReplicaMeanT16", "Expand16", "CrossReplicaMean")
 BATCH = -1  # unknown (batch) dimension, only allowed through Placeholder
 _NAME_RE = re.compile(r"^[A-Za-z0-9_./]+$")
 
@@ -267,3 +269,26 @@ class Graph:
     # ------------------------------------------------------------------- misc
     def to_json(self) -> str:
         return json.dumps({"version": 1, "nodes": [n.to_dict() for n in self.nodes]}, sort_keys=True)
+
+
+def insert_exchange(graph: Graph, world: int, exchange: str) -> Graph:
+    """Compression-insertion on the replica->combine transfer (PAPER.md :813-821 on the
+    §7 :934-941 channel; SPEC.md:681-689 shape).  For world > 1, between every
+    ApplyGradientDescent and its gradient: TRUNC16 -> Truncate16, CrossReplicaMeanT16
+    (attr world), Expand16; FP32 modes -> CrossReplicaMean.  world == 1 or NONE: a copy
+    (reading A6).  The replicas themselves are implicit (one per rank)."""
+    out = Graph()
+    active = world > 1 and exchange != "NONE"
+    for n in graph.nodes:
+        inputs = list(n.inputs)
+        if active and n.op == "ApplyGradientDescent":
+            var, g = inputs
+            G = out.by_name[g]
+            if exchange == "TRUNC16":
+                t = out._add(f"xchg/{var}/trunc16", "Truncate16", [g], {}, "u16", G.shape)
+                m = out._add(f"xchg/{var}/mean", "CrossReplicaMeanT16", [t], {"world": world}, "u16", G.shape)
+                inputs[1] = out._add(f"xchg/{var}/expand16", "Expand16", [m], {}, "f32", G.shape)
+            else:
+                inputs[1] = out._add(f"xchg/{var}/mean", "CrossReplicaMean", [g], {"world": world}, "f32", G.shape)
+        out._add(n.name, n.op, inputs, n.attrs, n.dtype, n.shape)
+    return out

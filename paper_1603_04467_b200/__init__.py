@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdflow.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_1603_04467_b200.build` "
+    raise ImportError(f"{LIB_PATH} is not built; run `python paper_1603_04467_b200/build.py` "
                       "(dflow has no CPU fallback)")
 _lib = C.CDLL(LIB_PATH)
 
@@ -74,6 +74,7 @@ _SIGS = {
     "dflow_gradients": (_i32, [_p, _node, _i32, _pnode, _pnode]),
     "dflow_apply_gradient_descent": (_i32, [_p, C.c_char_p, _node, C.c_float, _node, _pnode]),
     "dflow_graph_to_json": (_i32, [_p, C.c_char_p, _sz, C.POINTER(_sz)]),
+    "dflow_graph_insert_exchange": (_i32, [_p, _i32, _i32, C.POINTER(_p)]),
     "dflow_nccl_unique_id": (_i32, [C.POINTER(C.c_uint8)]),
     "dflow_session_create": (_i32, [_p, C.POINTER(dflow_options), C.POINTER(C.c_uint8), C.POINTER(_p)]),
     "dflow_session_destroy": (None, [_p]),
@@ -196,7 +197,6 @@ def mlp_graph(dims, loss: str = "MSE", lr: float = 0.25, with_dx: bool = False, 
     gout = (_node * len(xs))()
     check(dflow_gradients(g, cost, len(xs), node_array(xs), gout))
     grads = dict(zip(xs, list(gout)))
-    names = {}
     applies = []
     if train:
         for v in xs:

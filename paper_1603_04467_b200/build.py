@@ -1,6 +1,6 @@
 """Builds libdflow.so in-tree with nvcc for sm_100a (no JIT cache, no CPU fallback).
 
-    python -m paper_1603_04467_b200.build [--force]
+    python paper_1603_04467_b200/build.py [--force]     (or __graft_entry__.build())
 
 Every .cu/.cpp under csrc/ is compiled with
 ``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` (no --use_fast_math:

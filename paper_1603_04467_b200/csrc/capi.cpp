@@ -181,6 +181,23 @@ dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, si
   GUARD_END
 }
 
+dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int exchange, dflow_graph** out) {
+  GUARD_BEGIN
+  if (!g || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
+  if (world < 1 || exchange < DFLOW_EXCHANGE_TRUNC16 || exchange > DFLOW_EXCHANGE_NONE)
+    return fail(DFLOW_INVALID_ARGUMENT, "bad world/exchange");
+  dflow_graph* r = new dflow_graph();
+  std::vector<int> remap;
+  dflow_status st = dflow::insert_exchange(g->g, world, exchange, &r->g, &remap);
+  if (st != DFLOW_OK) {
+    delete r;
+    return st;
+  }
+  *out = r;
+  return DFLOW_OK;
+  GUARD_END
+}
+
 // ------------------------------------------------------------------ session
 dflow_status dflow_nccl_unique_id(uint8_t* out128) {
   if (!out128) return fail(DFLOW_INVALID_ARGUMENT, "out is NULL");
