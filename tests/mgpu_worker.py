@@ -1,0 +1,126 @@
+"""One rank of the N-GPU parity checks (launched by tests/test_gpu_multi.py via torchrun).
+
+Checks, for world = N GPUs over NCCL (§7 :934-941, §5.5 :813-821):
+  P4  exchange bit-exact: dflow_exchange(g_r) == oracle combine of the same g_r
+  P4' step bit-exact: W after dflow_train_step == oracle apply(oracle combine(trunc(g_r)))
+      where g_r are the GPU's own fp32 gradients of rank r (fetched, same kernels)
+  P11 every rank holds bitwise identical W, b after each step
+  gate W after one step vs the oracle's N-replica step within 2e-2 (bf16)
+Rank 0 writes a JSON verdict to argv[1].
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import paper_1603_04467_b200 as D  # noqa: E402
+from dflow_harness import Run, normwise, stream_ptr  # noqa: E402
+from oracle import kernels as OK  # noqa: E402
+from oracle.exchange import combine  # noqa: E402
+from oracle.mlp import build_mlp, train_step  # noqa: E402
+import synth  # noqa: E402
+
+
+def main(out_path, exchange):
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idt, 0)
+    nid = bytes(idt.cpu().numpy().tobytes())
+    verdict = {"world": world, "exchange": exchange}
+
+    w = synth.with_batch(synth.C2, 256)
+    b = w.batch // world
+    Ws, bs = synth.init_params(w)
+    X, Y = synth.batch(w)
+    Xr, Yr = X[rank * b:(rank + 1) * b], Y[rank * b:(rank + 1) * b]
+    run = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local, nccl_id=nid)
+    run.assign(Ws, bs)
+    Xd, Yd = torch.from_numpy(Xr).cuda(), torch.from_numpy(Yr).cuda()
+
+    # --- P4: exchange alone on random gradients (ragged length)
+    n = 100003
+    g_local = synth.rng(500 + rank).standard_normal(n).astype(np.float32)
+    gd = torch.from_numpy(g_local).cuda()
+    outd = torch.empty(n, dtype=torch.float32, device="cuda")
+    D.check(D.dflow_exchange(run.s, C.c_void_p(gd.data_ptr()), C.c_void_p(outd.data_ptr()), n, stream_ptr()))
+    torch.cuda.synchronize()
+    all_g = [synth.rng(500 + r).standard_normal(n).astype(np.float32) for r in range(world)]
+    ref = combine(all_g, exchange if exchange != "FP32_NCCL" else "FP32")
+    got = outd.cpu().numpy()
+    if exchange == "FP32_NCCL":
+        verdict["p4_exchange_max_rel"] = normwise(got, ref)
+        verdict["p4_exchange_ok"] = verdict["p4_exchange_max_rel"] < 1e-6
+    else:
+        verdict["p4_exchange_ok"] = bool(np.array_equal(got.view(np.uint32), ref.view(np.uint32)))
+
+    # --- per-rank GPU gradients, gathered on every rank
+    gW, gb, _ = run.gradients(Xd, Yd)
+    flat = np.concatenate([np.concatenate([a.ravel(), c.ravel()]) for a, c in zip(gW, gb)]).astype(np.float32)
+    t = torch.from_numpy(flat).cuda()
+    gathered = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(gathered, t)
+    per_rank = [x.cpu().numpy() for x in gathered]
+
+    # --- one train step
+    loss = run.step(Xd, Yd)
+    Wg, bg = run.read()
+    mine = np.concatenate([np.concatenate([a.ravel(), c.ravel()]) for a, c in zip(Wg, bg)])
+    mt = torch.from_numpy(mine).cuda()
+    allW = [torch.empty_like(mt) for _ in range(world)]
+    dist.all_gather(allW, mt)
+    verdict["p11_replicas_identical"] = all(bool(torch.equal(allW[0], x)) for x in allW)
+
+    # P4': oracle exchange + apply of the GPU's own gradients == the GPU step, bit for bit
+    if exchange in ("TRUNC16", "FP32"):
+        ok = True
+        off = 0
+        for l in range(w.layers):
+            for arr, var, lr in ((Ws[l], "W", w.lr), (bs[l], "b", w.lr)):
+                sz = arr.size
+                ghat = combine([p[off:off + sz] for p in per_rank], exchange).reshape(arr.shape)
+                new = OK.apply_gradient_descent(arr, lr, ghat, "f32")
+                gpu = Wg[l] if var == "W" else bg[l]
+                ok &= bool(np.array_equal(new.view(np.uint32), gpu.view(np.uint32)))
+                off += sz
+        verdict["p4_step_bitexact"] = ok
+
+    # gate: vs the oracle's N-replica step on the same global batch
+    mg = build_mlp(w.dims, "MSE", w.lr)
+    ref = train_step(mg, Ws, bs, X, Y, world, exchange if exchange != "FP32_NCCL" else "FP32")
+    errs = [normwise(a, r) for a, r in zip(Wg + bg, ref["W"] + ref["b"])]
+    verdict["w_after_max_err"] = max(errs)
+    verdict["loss_rel_err"] = abs(loss - ref["loss"]) / ref["loss"]
+
+    # a few more steps: replicas stay identical (P11)
+    for step in range(3):
+        Xs, Ys = synth.batch(w, step=step)
+        run.step(torch.from_numpy(Xs[rank * b:(rank + 1) * b]).cuda(),
+                 torch.from_numpy(Ys[rank * b:(rank + 1) * b]).cuda())
+    Wg, bg = run.read()
+    mine = np.concatenate([np.concatenate([a.ravel(), c.ravel()]) for a, c in zip(Wg, bg)])
+    mt = torch.from_numpy(mine).cuda()
+    dist.all_gather(allW, mt)
+    verdict["p11_after_4_steps"] = all(bool(torch.equal(allW[0], x)) for x in allW)
+    run.close()
+    if rank == 0:
+        with open(out_path, "w") as f:
+            json.dump(verdict, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "TRUNC16")

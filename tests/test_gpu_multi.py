@@ -1,0 +1,55 @@
+"""N-GPU parity over NCCL/NVLink (needs >= 2 GPUs; skipped on a 1-GPU box)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(n, exchange, tmp_path):
+    out = tmp_path / f"verdict_{n}_{exchange}.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tests", "mgpu_worker.py"), str(out), exchange]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return json.load(open(out))
+
+
+@pytest.mark.parametrize("exchange", ["TRUNC16", "FP32", "FP32_NCCL"])
+def test_two_gpu_replicated_step(exchange, tmp_path):
+    assert torch.cuda.is_available()
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    v = _run(2, exchange, tmp_path)
+    print(v)
+    assert v["p4_exchange_ok"], v
+    assert v["p11_replicas_identical"] and v["p11_after_4_steps"], v
+    if exchange != "FP32_NCCL":
+        assert v["p4_step_bitexact"], v
+    assert v["w_after_max_err"] < 2e-2, v
+
+
+def test_four_gpu_replicated_step(tmp_path):
+    assert torch.cuda.is_available()
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    v = _run(4, "TRUNC16", tmp_path)
+    print(v)
+    assert v["p4_exchange_ok"] and v["p4_step_bitexact"] and v["p11_after_4_steps"], v
+    assert v["w_after_max_err"] < 2e-2, v
