@@ -133,41 +133,6 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// One block per row slice (grid-stride over rows); each thread walks columns.
-__global__ void k_loss_seed(int kind, const float* __restrict__ a, int64_t lda, const float* __restrict__ y,
-                            int64_t ldy, int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ dz, int64_t lddz,
-                            float* __restrict__ dz32, int64_t lddz32, double* __restrict__ partials) {
-  const float denom = static_cast<float>(rows * cols);
-  const float inv_rows = __fdiv_rn(1.0f, static_cast<float>(rows));
-  double acc = 0.0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
-      const float av = a[r * lda + c];
-      float g;
-      if (kind == 0) {
-        const float d = __fsub_rn(av, y[r * ldy + c]);
-        acc += static_cast<double>(d) * static_cast<double>(d);
-        g = __fdiv_rn(d, denom);  // IEEE division (reading A20)
-      } else {
-        acc += static_cast<double>(av);
-        g = inv_rows;
-      }
-      const float v = (av > 0.f) ? g : 0.f;  // Relu'(a) with Relu'(0) = 0 (reading A10)
-      if (dz) dz[r * lddz + c] = __float2bfloat16_rn(v);
-      if (dz32) dz32[r * lddz32 + c] = v;
-    }
-  }
-  __shared__ double sm[32];
-  acc = warp_sum_d(acc);
-  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    double v = (threadIdx.x < (blockDim.x >> 5)) ? sm[threadIdx.x] : 0.0;
-    v = warp_sum_d(v);
-    if (threadIdx.x == 0) partials[blockIdx.x] = v;
-  }
-}
-
 __global__ void k_loss_final(int kind, const double* __restrict__ partials, int n, int64_t rows, int64_t cols,
                              float* __restrict__ loss) {
   double v = 0.0;
@@ -180,65 +145,32 @@ __global__ void k_loss_final(int kind, const double* __restrict__ partials, int 
   }
 }
 
-// ------------------------------------------------------------------ colsum
-// Block (x = 256-column slab, y = row chunk); thread = 8 consecutive columns x one of 8 row lanes.
-template <typename T>
-__global__ void k_colsum_partial(const T* __restrict__ dz, int64_t ld, int64_t rows, int64_t cols,
-                                 int64_t rows_per_chunk, float* __restrict__ ws, int vec) {
-  const int cg = threadIdx.x & 31, rl = threadIdx.x >> 5;
-  const int64_t c0 = blockIdx.x * 256 + cg * 8;
-  const int64_t r0 = blockIdx.y * rows_per_chunk;
-  const int64_t r1 = min(rows, r0 + rows_per_chunk);
-  float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const bool full = vec && (c0 + 8 <= cols);
-  for (int64_t r = r0 + rl; r < r1; r += 8) {
-    const T* p = dz + r * ld + c0;
-    if constexpr (sizeof(T) == 2) {
-      if (full) {
-        const uint4 v = *reinterpret_cast<const uint4*>(p);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16));
-        continue;
-      }
-    } else {
-      if (full) {
-        const float4 a = *reinterpret_cast<const float4*>(p);
-        const float4 b = *reinterpret_cast<const float4*>(p + 4);
-        const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], v[e]);
-        continue;
-      }
-    }
-#pragma unroll
-    for (int e = 0; e < 8; ++e)
-      if (c0 + e < cols) {
-        float x;
-        if constexpr (sizeof(T) == 2) x = __bfloat162float(p[e]); else x = p[e];
-        s[e] = __fadd_rn(s[e], x);
-      }
-  }
-  __shared__ float sm[8][256 + 8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) sm[rl][cg * 8 + e] = s[e];
-  __syncthreads();
-  const int c = threadIdx.x;
-  if (blockIdx.x * 256 + c < cols) {
-    float t = sm[0][c];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) t = __fadd_rn(t, sm[k][c]);
-    ws[blockIdx.y * cols + blockIdx.x * 256 + c] = t;
-  }
-}
-
+// ------------------------------------------------------------------ colsum (final pass)
+// Block = 32 columns x 8 chunk-groups; group g sums chunks g, g+8, ... in order, then
+// the 8 group sums are added in group order (deterministic, ~#chunks/8 dependent adds).
 __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols, float* __restrict__ out32,
                                uint16_t* __restrict__ out16) {
-  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
-    float t = ws[c];
-    for (int k = 1; k < chunks; ++k) t = __fadd_rn(t, ws[k * cols + c]);
-    if (out32) out32[c] = t;
-    if (out16) out16[c] = static_cast<uint16_t>(__float_as_uint(t) >> 16);
+  __shared__ float sm[8][33];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32LL + cl;
+  float t = 0.f;
+  if (c < cols) {
+    int k = g;
+    for (; k + 24 < chunks; k += 32) {  // 4 independent loads in flight, added in order
+      const float a0 = ws[(int64_t)k * cols + c], a1 = ws[(int64_t)(k + 8) * cols + c];
+      const float a2 = ws[(int64_t)(k + 16) * cols + c], a3 = ws[(int64_t)(k + 24) * cols + c];
+      t = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(t, a0), a1), a2), a3);
+    }
+    for (; k < chunks; k += 8) t = __fadd_rn(t, ws[(int64_t)k * cols + c]);
+  }
+  sm[g][cl] = t;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float s = sm[0][cl];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
+    if (out32) out32[c] = s;
+    if (out16) out16[c] = static_cast<uint16_t>(__float_as_uint(s) >> 16);
   }
 }
 
@@ -393,42 +325,17 @@ cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat1
   return cudaGetLastError();
 }
 
-cudaError_t launch_loss_seed(int kind, const float* a, int64_t lda, const float* y, int64_t ldy, int64_t rows,
-                             int64_t cols, __nv_bfloat16* dz, int64_t lddz, float* dz32, int64_t lddz32,
-                             double* partials, float* loss_dev, cudaStream_t s) {
-  k_loss_seed<<<kLossBlocks, kThreads, 0, s>>>(kind, a, lda, y, ldy, rows, cols, dz, lddz, dz32, lddz32, partials);
-  k_loss_final<<<1, 32, 0, s>>>(kind, partials, kLossBlocks, rows, cols, loss_dev);
+cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t rows, int64_t cols, float* loss,
+                              cudaStream_t s) {
+  k_loss_final<<<1, 32, 0, s>>>(kind, partials, n, rows, cols, loss);
   return cudaGetLastError();
 }
 
-int colsum_rowchunks(int64_t rows, int64_t cols) {
-  const int64_t slabs = (cols + 255) / 256;
-  int64_t chunks = (148 * 4 + slabs - 1) / slabs;
-  chunks = std::min<int64_t>(chunks, std::max<int64_t>(1, (rows + 63) / 64));
-  return static_cast<int>(std::max<int64_t>(chunks, 1));
-}
-
-template <typename T>
-static cudaError_t colsum_impl(const T* dz, int64_t ld, int64_t rows, int64_t cols, float* ws, float* out_f32,
-                               uint16_t* out_u16, cudaStream_t s) {
+cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
+                                cudaStream_t s) {
   if (cols == 0) return cudaSuccess;
-  const int chunks = colsum_rowchunks(rows, cols);
-  const int64_t rpc = (rows + chunks - 1) / chunks;
-  const int vec = al16(dz) && ((ld * (int64_t)sizeof(T)) % 16 == 0);
-  dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>(chunks));
-  k_colsum_partial<T><<<grid, 256, 0, s>>>(dz, ld, rows, cols, rpc > 0 ? rpc : 1, ws, vec);
-  k_colsum_final<<<blocks_for(cols), kThreads, 0, s>>>(ws, chunks, cols, out_f32, out_u16);
+  k_colsum_final<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16);
   return cudaGetLastError();
-}
-
-cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int64_t ld, int64_t rows, int64_t cols, float* ws,
-                               float* out_f32, uint16_t* out_u16, cudaStream_t s) {
-  return colsum_impl(dz, ld, rows, cols, ws, out_f32, out_u16, s);
-}
-
-cudaError_t launch_colsum_f32(const float* dz, int64_t ld, int64_t rows, int64_t cols, float* ws, float* out_f32,
-                              uint16_t* out_u16, cudaStream_t s) {
-  return colsum_impl(dz, ld, rows, cols, ws, out_f32, out_u16, s);
 }
 
 cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,

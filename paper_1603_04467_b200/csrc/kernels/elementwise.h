@@ -18,23 +18,16 @@ cudaError_t launch_cast_bf16(const float* src, int64_t lds, __nv_bfloat16* dst, 
 cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
                              int64_t cols, cudaStream_t s);
 
-// NK7: loss and gradient seed from the last activation a (fp32).
-//   MSE: d = a - y;  dz = 1[a>0] * d / (rows*cols);  C = sum(d^2) / (2 rows cols)
-//   SUM:             dz = 1[a>0] * (1 / rows);       C = sum(a) / rows
-// Writes dz (bf16) and/or dz32 (fp32); the loss lands in *loss_dev (fp32) via
-// a deterministic two-pass reduction (fixed grid, fixed order).
-constexpr int kLossBlocks = 296;
-cudaError_t launch_loss_seed(int kind, const float* a, int64_t lda, const float* y, int64_t ldy, int64_t rows,
-                             int64_t cols, __nv_bfloat16* dz, int64_t lddz, float* dz32, int64_t lddz32,
-                             double* partials /*[kLossBlocks]*/, float* loss_dev, cudaStream_t s);
+// NK7 final pass: the last forward GEMM's epilogue (EPI_BIAS_RELU_LOSS) leaves
+// n per-(CTA, warp) partial sums; C = sum / (2 rows cols) (MSE) or sum / rows
+// (SUM), summed in a fixed order (deterministic) into *loss (fp32).
+cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t rows, int64_t cols, float* loss,
+                              cudaStream_t s);
 
-// NK8: db[c] = sum_r dz[r, c] (bf16 input, fp32 accumulate, fixed order).
-// Outputs fp32 and/or trunc16 (u16).  ws: rowchunks*cols floats scratch.
-int colsum_rowchunks(int64_t rows, int64_t cols);
-cudaError_t launch_colsum_bf16(const __nv_bfloat16* dz, int64_t ld, int64_t rows, int64_t cols, float* ws,
-                               float* out_f32, uint16_t* out_u16, cudaStream_t s);
-cudaError_t launch_colsum_f32(const float* dz, int64_t ld, int64_t rows, int64_t cols, float* ws, float* out_f32,
-                              uint16_t* out_u16, cudaStream_t s);
+// NK8 final pass: db[c] = sum_k ws[k, c] over the `chunks` per-32-row partial
+// column sums the dz-producing epilogue wrote (fixed order).  fp32 and/or u16 out.
+cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
+                                cudaStream_t s);
 
 // NK11: owner fold of N received shards (rank order), x (1/N), truncate.
 cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,

@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -71,6 +72,7 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi) {
   if (!a_mn && b_mn) {
     if (epi == EPI_BIAS_RELU) return kernel_ptr<BN, CG, false, true, EPI_BIAS_RELU>();
     if (epi == EPI_F32) return kernel_ptr<BN, CG, false, true, EPI_F32>();
+    if (epi == EPI_BIAS_RELU_LOSS) return kernel_ptr<BN, CG, false, true, EPI_BIAS_RELU_LOSS>();
   } else if (!a_mn && !b_mn) {
     if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, false, false, EPI_RELUGRAD>();
     if (epi == EPI_F32) return kernel_ptr<BN, CG, false, false, EPI_F32>();
@@ -79,6 +81,23 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi) {
     if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, true, true, EPI_TRUNC16>();
   }
   return nullptr;
+}
+
+// Per-device tile-scheduler counters [counter, done]; zeroed once, and every GEMM
+// launch leaves them zero again, so launches serialised on a stream can share them.
+static int* default_sched() {
+  static int* ptrs[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!ptrs[dev]) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    ptrs[dev] = static_cast<int*>(p);
+  }
+  return ptrs[dev];
 }
 
 static bool aligned16(const void* p, int64_t ld, int elem) {
@@ -137,9 +156,28 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.vec_out = aligned16(d.out, d.ldo, out_elem) ? 1 : 0;
   a.vec_out32 = aligned16(d.out_f32, d.ldo32, 4) ? 1 : 0;
   a.vec_mask = aligned16(d.mask, d.ldm, 2) ? 1 : 0;
+  a.y = d.y;
+  a.ldy = d.ldy;
+  a.loss_kind = d.loss_kind;
+  a.loss_denom = static_cast<float>(d.M * d.N);
+  const int64_t mn = d.M * d.N;
+  a.denom_pow2 = (mn > 0 && (mn & (mn - 1)) == 0) ? 1 : 0;
+  a.inv_denom = 1.0f / a.loss_denom;
+  a.vec_y = aligned16(d.y, d.ldy, 4) ? 1 : 0;
+  a.group_m = 16;
+  if (const char* e = getenv("DFLOW_GEMM_GROUP")) a.group_m = atoi(e) > 0 ? atoi(e) : 16;
+  a.sched = default_sched();
+  if (!a.sched) {
+    snprintf(g_err, sizeof g_err, "could not allocate the tile-scheduler counters");
+    return cudaErrorMemoryAllocation;
+  }
+  a.seed_const = 1.0f / static_cast<float>(d.M);
+  a.loss_partials = d.loss_partials;
+  a.colsum_ws = d.colsum_ws;
   if ((d.epilogue == EPI_F32 && !d.out_f32) || (d.epilogue == EPI_TRUNC16 && !d.out) ||
       (d.epilogue == EPI_RELUGRAD && (!d.out || !d.mask)) ||
-      (d.epilogue == EPI_BIAS_RELU && (!d.bias || (!d.out && !d.out_f32)))) {
+      (d.epilogue == EPI_BIAS_RELU && (!d.bias || (!d.out && !d.out_f32))) ||
+      (d.epilogue == EPI_BIAS_RELU_LOSS && (!d.bias || !d.out || (d.loss_kind == 0 && !d.y)))) {
     snprintf(g_err, sizeof g_err, "missing GEMM epilogue operand (epi=%d)", d.epilogue);
     return cudaErrorInvalidValue;
   }

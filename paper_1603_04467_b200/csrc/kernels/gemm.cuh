@@ -41,18 +41,18 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;       // two accumulator buffers
-  static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
+  static constexpr int BAR_BYTES = (2 * STAGES + 8) * 8 + 32;
+  static constexpr int SCHED_CONSUMERS = (CG == 2) ? 11 : 6;  // producer x CG + MMA + 4 epilogue warps x CG
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + alignment slack
   static_assert(TMEM_COLS >= 32 && TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "tmem cols");
   static_assert(BN % 32 == 0 && BN_CTA % 64 == 0, "tile N");
 };
 
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
-  constexpr int GROUP = 8;
-  const int per_group = GROUP * tiles_n;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int& tm, int& tn) {
+  const int per_group = group * tiles_n;
   const int g = t / per_group;
-  const int first_m = g * GROUP;
-  const int gsize = min(tiles_m - first_m, GROUP);
+  const int first_m = g * group;
+  const int gsize = min(tiles_m - first_m, group);
   const int r = t - g * per_group;
   tm = first_m + r % gsize;
   tn = r / gsize;
@@ -80,7 +80,10 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+  uint64_t* sched_full = bars + 2 * STAGES + 4;   // [2] tile id published (count 1)
+  uint64_t* sched_empty = bars + 2 * STAGES + 6;  // [2] tile id consumed (leader; SCHED_CONSUMERS arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
+  int* sched_tile = reinterpret_cast<int*>(tmem_slot + 4);  // [2]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -89,6 +92,25 @@ __global__ void __launch_bounds__(256, 1)
   const int num_clusters = gridDim.x / CG;
   const int num_tiles = args.tiles_m * args.tiles_n;
   const int num_kb = (args.K + BK - 1) / BK;
+
+  // Dynamic tile scheduler: the leader CTA's warp 3 draws tile ids from a global
+  // atomic counter (first tile = cluster id) and publishes them through a 2-deep
+  // smem ring in every CTA of the cluster, so the set of tiles in flight stays a
+  // contiguous window of the M-grouped raster (L2 reuse) even when SMs drift.
+  const uint32_t sched_empty_leader =
+      (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&sched_empty[0]), 0) : ptx::smem_u32(&sched_empty[0]);
+  auto next_tile = [&](int& slot, uint32_t& ph, bool whole_warp) -> int {
+    ptx::mbar_wait_cluster(ptx::smem_u32(&sched_full[slot]), ph);
+    const int t = *reinterpret_cast<volatile int*>(&sched_tile[slot]);
+    if (whole_warp) __syncwarp();
+    if (!whole_warp || lane == 0) {
+      if constexpr (CG == 2) ptx::mbar_arrive_cluster(sched_empty_leader + slot * 8);
+      else ptx::mbar_arrive(ptx::smem_u32(&sched_empty[slot]));
+    }
+    slot ^= 1;
+    if (slot == 0) ph ^= 1;
+    return t;
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -102,6 +124,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(ptx::smem_u32(&tfull[a]), 1);
       ptx::mbar_init(ptx::smem_u32(&tempty[a]), 4 * CG);
+      ptx::mbar_init(ptx::smem_u32(&sched_full[a]), 1);
+      ptx::mbar_init(ptx::smem_u32(&sched_empty[a]), Cfg::SCHED_CONSUMERS);
     }
     ptx::fence_mbarrier_init();
   }
@@ -113,14 +137,18 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     // ===================== TMA producer =====================
-    if (lane == 0 && num_kb > 0) {
+    if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int sslot = 0;
+      uint32_t sph = 0;
       const uint32_t full0_local = ptx::smem_u32(&full[0]);
       const uint32_t full0 = (CG == 2) ? ptx::mapa_shared(full0_local, 0) : full0_local;
-      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      for (;;) {
+        const int t = next_tile(sslot, sph, false);
+        if (t >= num_tiles) break;
         int tm, tn;
-        tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+        tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
         const int m0 = tm * (BM * CG) + cta_rank * BM;
         const int n0 = tn * BN + cta_rank * BN_CTA;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -152,13 +180,18 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread of the leader CTA) =====================
-    if (cta_rank == 0 && lane == 0 && num_kb > 0) {
+    if (cta_rank == 0 && lane == 0) {
       constexpr uint32_t idesc = ptx::make_idesc(BM * CG, BN, A_MN, B_MN, false);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+      int sslot = 0;
+      uint32_t sph = 0;
+      for (;;) {
+        const int t = next_tile(sslot, sph, false);
+        if (t >= num_tiles) break;
+        if (num_kb == 0) continue;
         ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
@@ -183,6 +216,37 @@ __global__ void __launch_bounds__(256, 1)
         if (acc == 0) acc_phase ^= 1;
       }
     }
+  } else if (warp == 3) {
+    // ===================== tile scheduler (one thread of the leader CTA) =====================
+    if (cta_rank == 0 && lane == 0) {
+      int slot = 0;
+      uint32_t ph = 0;
+      int t = cluster_id;
+      for (;;) {
+        ptx::mbar_wait(ptx::smem_u32(&sched_empty[slot]), ph ^ 1);
+#pragma unroll
+        for (int r = 0; r < CG; ++r) {
+          const uint32_t tile_addr = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&sched_tile[slot]), r)
+                                               : ptx::smem_u32(&sched_tile[slot]);
+          const uint32_t full_addr = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&sched_full[slot]), r)
+                                               : ptx::smem_u32(&sched_full[slot]);
+          ptx::st_shared_cluster(tile_addr, static_cast<uint32_t>(t));
+          ptx::mbar_arrive_cluster(full_addr);
+        }
+        if (t >= num_tiles) break;
+        t = args.sched ? num_clusters + atomicAdd(&args.sched[0], 1) : t + num_clusters;
+        slot ^= 1;
+        if (slot == 0) ph ^= 1;
+      }
+      if (args.sched) {
+        // the last cluster to finish resets the counters for the next launch on this stream
+        __threadfence();
+        if (atomicAdd(&args.sched[1], 1) == num_clusters - 1) {
+          atomicExch(&args.sched[0], 0);
+          atomicExch(&args.sched[1], 0);
+        }
+      }
+    }
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> registers -> global =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
@@ -190,9 +254,14 @@ __global__ void __launch_bounds__(256, 1)
         (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0) : ptx::smem_u32(&tempty[0]);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+    double loss_acc = 0.0;
+    int sslot = 0;
+    uint32_t sph = 0;
+    for (;;) {
+      const int t = next_tile(sslot, sph, true);
+      if (t >= num_tiles) break;
       int tm, tn;
-      tile_coords(t, args.tiles_m, args.tiles_n, tm, tn);
+      tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
       const int gm = tm * (BM * CG) + cta_rank * BM + q * 32 + lane;
       const bool row_ok = gm < args.M;
       if (num_kb > 0) {
@@ -269,35 +338,118 @@ __global__ void __launch_bounds__(256, 1)
               for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = v[j];
             }
           }
-        } else if constexpr (EPI == EPI_RELUGRAD) {
-          const __nv_bfloat16* mrow = reinterpret_cast<const __nv_bfloat16*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
-          if (full_chunk && args.vec_out && args.vec_mask) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j));
-              const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                // bf16 > 0  <=>  sign bit clear and not +0 (and not NaN)
-                const bool pos = (h & 0x8000u) == 0 && h != 0 && h <= 0x7F80u;
-                v[e] = pos ? u32_as_f32(r[j + e]) : 0.f;
-              }
-              *reinterpret_cast<uint4*>(o + j) = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                                                            pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (gn + j >= args.N) continue;
-              const float mj = __bfloat162float(mrow[j]);
-              o[j] = __float2bfloat16_rn(mj > 0.f ? u32_as_f32(r[j]) : 0.f);
-            }
-          }
         }
         }  // row_ok && gn < N
+        if constexpr (EPI == EPI_RELUGRAD || EPI == EPI_BIAS_RELU_LOSS) {
+          // dz values as stored (bf16-rounded), 0 outside the matrix; fused column sums.
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          if (row_ok && gn < args.N) {
+            const bool full_chunk = gn + 32 <= args.N;
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+            if constexpr (EPI == EPI_RELUGRAD) {
+              const __nv_bfloat16* mrow =
+                  reinterpret_cast<const __nv_bfloat16*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
+              if (full_chunk && args.vec_mask) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                  const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j));
+                  const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                    // bf16 > 0  <=>  sign bit clear, not +0, not NaN
+                    const bool pos = (h & 0x8000u) == 0 && h != 0 && h <= 0x7F80u;
+                    v[j + e] = pos ? u32_as_f32(r[j + e]) : 0.f;
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (gn + j < args.N) v[j] = (__bfloat162float(mrow[j]) > 0.f) ? u32_as_f32(r[j]) : 0.f;
+              }
+            } else {  // EPI_BIAS_RELU_LOSS: a = relu(acc + b); loss seed (reading A2, A10, A20)
+              const float* yrow = args.y + static_cast<int64_t>(gm) * args.ldy + gn;
+              float* o32 = args.out_f32 ? args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn : nullptr;
+              // issue all 32 target loads up front (vectorised when aligned)
+              float yv[32];
+              if (args.loss_kind == 0) {
+                if (full_chunk && args.vec_y) {
+#pragma unroll
+                  for (int j = 0; j < 32; j += 4) {
+                    const float4 t4 = __ldg(reinterpret_cast<const float4*>(yrow + j));
+                    yv[j] = t4.x; yv[j + 1] = t4.y; yv[j + 2] = t4.z; yv[j + 3] = t4.w;
+                  }
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j) yv[j] = (gn + j < args.N) ? __ldg(yrow + j) : 0.f;
+                }
+              }
+              float part = 0.f;  // this chunk's loss contribution (fp32), folded into loss_acc (fp64)
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const bool in = gn + j < args.N;
+                const float z = __fadd_rn(u32_as_f32(r[j]), in ? __ldg(args.bias + gn + j) : 0.f);
+                const float a = (z < 0.f) ? 0.f : z;
+                float g;
+                if (args.loss_kind == 0) {  // MSE: d = a - y, g = d / (rows*cols) (IEEE, reading A20)
+                  const float d = __fsub_rn(a, yv[j]);
+                  part = in ? __fmaf_rn(d, d, part) : part;
+                  g = args.denom_pow2 ? __fmul_rn(d, args.inv_denom) : __fdiv_rn(d, args.loss_denom);
+                } else {                    // SUM: g = 1 / rows
+                  part = in ? __fadd_rn(part, a) : part;
+                  g = args.seed_const;
+                }
+                yv[j] = a;
+                v[j] = (in && a > 0.f) ? g : 0.f;
+              }
+              loss_acc += static_cast<double>(part);
+              if (o32) {
+                if (full_chunk && args.vec_out32) {
+#pragma unroll
+                  for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4*>(o32 + j) = make_float4(yv[j], yv[j + 1], yv[j + 2], yv[j + 3]);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 32; ++j)
+                    if (gn + j < args.N) o32[j] = yv[j];
+                }
+              }
+            }
+            // round to the stored bf16 and store
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+            if (full_chunk && args.vec_out) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8)
+                *reinterpret_cast<uint4*>(o + j) =
+                    make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                               pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (gn + j < args.N) o[j] = __float2bfloat16_rn(v[j]);
+            }
+          }
+          if (args.colsum_ws != nullptr) {
+            // transpose-reduce: after 5 butterfly steps lane l holds the sum over this
+            // warp's 32 rows of column gn + l (fixed order -> deterministic)
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) {
+              const bool upper = (lane & off) != 0;
+#pragma unroll
+              for (int i = 0; i < off; ++i) {
+                const float send = upper ? v[i] : v[i + off];
+                const float keep = upper ? v[i + off] : v[i];
+                v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, off));
+              }
+            }
+            const int rowblk = (tm * (BM * CG) + cta_rank * BM + q * 32) >> 5;
+            if (gn + lane < args.N && rowblk * 32 < args.M)
+              args.colsum_ws[static_cast<int64_t>(rowblk) * args.N + gn + lane] = v[0];
+          }
+        }
         __syncwarp();
       }
       if (num_kb > 0) {
@@ -310,6 +462,11 @@ __global__ void __launch_bounds__(256, 1)
       }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
+    }
+    if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+      if (lane == 0 && args.loss_partials) args.loss_partials[blockIdx.x * 4 + q] = loss_acc;
     }
   }
 

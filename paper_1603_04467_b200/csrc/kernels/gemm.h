@@ -10,7 +10,9 @@ enum GemmEpilogue : int {
   EPI_F32 = 0,        // out_f32[m,n] = acc
   EPI_TRUNC16 = 1,    // out_u16[m,n] = bits(acc) >> 16              (a4 + a6 fused)
   EPI_BIAS_RELU = 2,  // a = relu(acc + bias[n]); out_bf16 (RNE) and/or out_f32  (a1)
-  EPI_RELUGRAD = 3,   // out_bf16 = acc * 1[mask_bf16[m,n] > 0]        (a3)
+  EPI_RELUGRAD = 3,   // out_bf16 = acc * 1[mask_bf16[m,n] > 0]        (a3) [+ fused db partials]
+  EPI_BIAS_RELU_LOSS = 4,  // a = relu(acc + bias) [-> out_f32]; loss seed dz -> out_bf16 (a1 + a2)
+                           // [+ fused db partials, + loss partials]
 };
 
 // Kernel arguments (by value, __grid_constant__-style).
@@ -27,6 +29,20 @@ struct GemmArgs {
   int vec_out;            // 1: 16-byte vector stores are aligned for out
   int vec_out32;          // 1: 16-byte vector stores are aligned for out_f32
   int vec_mask;           // 1: 16-byte vector loads are aligned for mask
+  // EPI_BIAS_RELU_LOSS
+  const float* y;         // target [M, ldy] (MSE)
+  int64_t ldy;
+  int loss_kind;          // 0 MSE, 1 SUM
+  float loss_denom;       // rows * cols (MSE seed divisor, IEEE division)
+  float inv_denom;        // 1 / loss_denom, exact when denom_pow2
+  int denom_pow2;         // 1: loss_denom is a power of two, so d * inv_denom == d / loss_denom
+  int vec_y;              // 1: 16-byte vector loads are aligned for y
+  int group_m;            // tile raster: M-tiles per group (L2 reuse of the B panels)
+  int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
+  float seed_const;       // 1 / rows (SUM seed)
+  double* loss_partials;  // [grid * 4] per-(CTA, epilogue warp) partial sums
+  // EPI_RELUGRAD / EPI_BIAS_RELU_LOSS: column sums of the stored dz per 32-row block
+  float* colsum_ws;       // [ceil(M / 32), N] or nullptr
 };
 
 struct GemmDesc {
@@ -38,6 +54,10 @@ struct GemmDesc {
   float* out_f32; int64_t ldo32;
   const float* bias;
   const void* mask; int64_t ldm;
+  const float* y; int64_t ldy;              // EPI_BIAS_RELU_LOSS
+  int loss_kind;
+  double* loss_partials;
+  float* colsum_ws;                         // fused db partials (RELUGRAD, BIAS_RELU_LOSS)
   int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair), 3 = 128x256 (1 CTA)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)
 };

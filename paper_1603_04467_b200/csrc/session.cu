@@ -4,10 +4,10 @@
 // Step schedule for rank r (local batch b = B/N, reading A4):
 //   cast x -> A0 (bf16)                                   NK13
 //   l = 1..L:  A_l = relu(A_{l-1} W_l + b_l)              NK1 (tcgen05 GEMM, fused epilogue)
-//   dZ_L, C_r = loss seed(A_L, y)                         NK7
-//   l = L..1:  dZ_{l-1} = (dZ_l W_l^T) . 1[A_{l-1} > 0]   NK2 (l > 1)
+//              (l = L: + loss seed dZ_L, C_r partials and db_L partials, NK7 fused)
+//   l = L..1:  dZ_{l-1} = (dZ_l W_l^T) . 1[A_{l-1} > 0]   NK2 (l > 1; + db_{l-1} partials fused)
 //              dW_l = A_{l-1}^T dZ_l  [-> trunc16]        NK3
-//              db_l = colsum(dZ_l)    [-> trunc16]        NK8
+//              db_l = sum of the per-32-row partials [-> trunc16]   NK8 (final pass)
 //              comm stream: alltoall -> owner fold -> allgather (NCCL, NVLink)   NK11
 //              W_l, b_l <- W - lr * expand(g_hat)         NK12
 #include "session.h"
@@ -228,7 +228,7 @@ dflow_status alloc_state(dflow_session* s) {
   const int64_t cap = s->cap;
   s->ld_A0 = pad_to(s->layers[0].in, 8);
   ST(dmalloc(s, &s->A0, cap * s->ld_A0));
-  int64_t ws = 0, max_out = 0;
+  int64_t max_out = 0;
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     ly.ld_out = pad_to(ly.out, 8);
@@ -242,6 +242,7 @@ dflow_status alloc_state(dflow_session* s) {
     ly.Ppad = pad_to(ly.P, 8 * N);
     ly.shard = ly.Ppad / N;
     ST(dmalloc(s, &ly.g32, ly.Ppad));
+    ST(dmalloc(s, &ly.colsum_ws, ((cap + 31) / 32) * ly.out));
     if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
       ST(dmalloc(s, &ly.q16, ly.Ppad));
       uint16_t *r, *o, *gt;
@@ -256,13 +257,11 @@ dflow_status alloc_state(dflow_session* s) {
       ST(dmalloc(s, &gt, ly.Ppad));
       ly.recv = r; ly.own = o; ly.gath = gt;
     }
-    ws = std::max<int64_t>(ws, static_cast<int64_t>(colsum_rowchunks(cap, ly.out)) * ly.out);
     max_out = std::max(max_out, ly.out);
   }
   s->ld_AL32 = pad_to(s->layers[s->L - 1].out, 4);
   ST(dmalloc(s, &s->AL32, cap * s->ld_AL32));
-  ST(dmalloc(s, &s->colsum_ws, ws));
-  ST(dmalloc(s, &s->loss_partials, kLossBlocks));
+  ST(dmalloc(s, &s->loss_partials, 4 * 1024));
   ST(dmalloc(s, &s->loss_dev, 4));
   s->mask_words_cap = (cap * std::max(max_out, s->layers[0].in) + 31) / 32;
   ST(dmalloc(s, &s->mask_dev, s->mask_words_cap));
@@ -300,12 +299,29 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     f.M = rows; f.N = ly.out; f.K = ly.in;
     f.A = Aprev; f.lda = ld_prev; f.a_mn = false;
     f.B = ly.Wbf; f.ldb = ly.ld_wb; f.b_mn = true;
-    f.epilogue = EPI_BIAS_RELU;
-    f.out = last ? nullptr : ly.A; f.ldo = ly.ld_out;
-    f.out_f32 = last ? s->AL32 : nullptr; f.ldo32 = s->ld_AL32;
     f.bias = ly.b32;
     f.max_ctas = max_ctas;
-    ST(gemm_plan(s, f, &ly.fwd));
+    if (!last) {
+      f.epilogue = EPI_BIAS_RELU;
+      f.out = ly.A; f.ldo = ly.ld_out;
+      ST(gemm_plan(s, f, &ly.fwd));
+    } else {
+      // last layer: Relu + loss seed + db partials fused (a1 + a2 + a5); y is patched per call
+      f.epilogue = EPI_BIAS_RELU_LOSS;
+      f.out = ly.dZ; f.ldo = ly.ld_out;
+      f.loss_kind = s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1;
+      f.y = s->AL32; f.ldy = s->ld_AL32;  // placeholder pointer, replaced at launch
+      f.loss_partials = s->loss_partials;
+      f.colsum_ws = ly.colsum_ws;
+      ST(gemm_plan(s, f, &ly.fwd));
+      f.out_f32 = s->AL32; f.ldo32 = s->ld_AL32;  // fetch variant also keeps fp32 A_L
+      ST(gemm_plan(s, f, &ly.fwd_fetch));
+      GemmDesc p = f;  // forward-only without a target: plain Relu, fp32 A_L
+      p.epilogue = EPI_BIAS_RELU;
+      p.out = nullptr;
+      p.y = nullptr; p.loss_partials = nullptr; p.colsum_ws = nullptr;
+      ST(gemm_plan(s, p, &ly.fwd_plain));
+    }
     ly.has_fwd = true;
     if (l > 0) {
       const Layer& lp = s->layers[l - 1];
@@ -316,6 +332,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.epilogue = EPI_RELUGRAD;
       d.out = lp.dZ; d.ldo = lp.ld_out;
       d.mask = lp.A; d.ldm = lp.ld_out;
+      d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
@@ -421,7 +438,9 @@ dflow_status check_rows(dflow_session* s, int64_t rows) {
 }
 
 // ------------------------------------------------------------------ phases
-dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStream_t st) {
+enum FwdMode { FWD_TRAIN = 0, FWD_FETCH = 1, FWD_ONLY = 2 };
+
+dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStream_t st, int mode) {
   if (!f.x) return fail(DFLOW_INVALID_ARGUMENT, "x must be fed");
   const int64_t in = s->layers[0].in;
   if (f.ldx < in) return fail(DFLOW_INVALID_ARGUMENT, "ld of x < its width");
@@ -432,21 +451,28 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
                                          st);
   tend(s, t, st);
   ST(check_launch(s, e, 1, "input cast"));
-  for (int l = 0; l < s->L; ++l) ST(launch_gemm(s, s->layers[l].fwd, st));
+  for (int l = 0; l + 1 < s->L; ++l) ST(launch_gemm(s, s->layers[l].fwd, st));
+  // last layer: Relu + loss seed (+ db_L partials) fused into the GEMM epilogue (a1+a2+a5)
+  Layer& last = s->layers[s->L - 1];
+  const bool need_y = s->loss_kind == DFLOW_LOSS_MSE;
+  if (mode == FWD_ONLY && need_y && !f.y) {
+    ST(launch_gemm(s, last.fwd_plain, st));  // forward fetch without a target: no loss
+  } else {
+    if (need_y && !f.y) return fail(DFLOW_INVALID_ARGUMENT, "y must be fed (MSE loss)");
+    if (need_y && f.ldy < last.out) return fail(DFLOW_INVALID_ARGUMENT, "ld of y < its width");
+    GemmPlan& p = (mode == FWD_TRAIN) ? last.fwd : last.fwd_fetch;
+    p.args.y = f.y;
+    p.args.ldy = f.ldy;
+    ST(launch_gemm(s, p, st));
+    const int t = tbegin(s, 1, st);
+    cudaError_t e2 = launch_loss_final(s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1, s->loss_partials, p.grid * 4, rows,
+                                       last.out, s->loss_dev, st);
+    tend(s, t, st);
+    ST(check_launch(s, e2, 1, "loss reduction"));
+  }
   s->have_forward = true;
   s->last_rows = rows;
   return DFLOW_OK;
-}
-
-dflow_status run_loss(dflow_session* s, const Feeds& f, int64_t rows, cudaStream_t st) {
-  const Layer& last = s->layers[s->L - 1];
-  if (s->loss_kind == DFLOW_LOSS_MSE && !f.y) return fail(DFLOW_INVALID_ARGUMENT, "y must be fed (MSE loss)");
-  if (s->loss_kind == DFLOW_LOSS_MSE && f.ldy < last.out) return fail(DFLOW_INVALID_ARGUMENT, "ld of y < its width");
-  const int t = tbegin(s, 1, st);
-  cudaError_t e = launch_loss_seed(s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1, s->AL32, s->ld_AL32, f.y, f.ldy, rows,
-                                   last.out, last.dZ, last.ld_out, nullptr, 0, s->loss_partials, s->loss_dev, st);
-  tend(s, t, st);
-  return check_launch(s, e, 2, "loss seed");
 }
 
 // Exchange + apply of layer l (comm stream when N > 1).
@@ -508,11 +534,13 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     Layer& ly = s->layers[l];
     if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
     ST(launch_gemm(s, t16 ? ly.wgrad16 : ly.wgrad32, st));
+    // db_l: the producing epilogue left per-32-row column partials; sum them in order
     const int t = tbegin(s, 1, st);
-    cudaError_t e = launch_colsum_bf16(ly.dZ, ly.ld_out, rows, ly.out, s->colsum_ws, t16 ? nullptr : ly.g32 + ly.in * ly.out,
-                                       t16 ? ly.q16 + ly.in * ly.out : nullptr, st);
+    cudaError_t e = launch_colsum_final(ly.colsum_ws, static_cast<int>((rows + 31) / 32), ly.out,
+                                        t16 ? nullptr : ly.g32 + ly.in * ly.out,
+                                        t16 ? ly.q16 + ly.in * ly.out : nullptr, st);
     tend(s, t, st);
-    ST(check_launch(s, e, 2, "bias-gradient column sum"));
+    ST(check_launch(s, e, 1, "bias-gradient column sum"));
     if (mode == 0) ST(exchange_apply(s, l, st));
   }
   if (mode == 0 && s->opt.world > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
@@ -626,11 +654,10 @@ void session_destroy(dflow_session* s) {
   if (s->nccl) ncclCommDestroy(s->nccl);
   for (Layer& ly : s->layers) {
     for (void* p : {(void*)ly.W32, (void*)ly.Wbf, (void*)ly.b32, (void*)ly.A, (void*)ly.dZ, (void*)ly.g32,
-                    (void*)ly.q16, ly.recv, ly.own, ly.gath})
+                    (void*)ly.q16, ly.recv, ly.own, ly.gath, (void*)ly.colsum_ws})
       if (p) cudaFree(p);
   }
-  for (void* p : {(void*)s->A0, (void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->colsum_ws,
-                  (void*)s->mask_dev, s->host_stage[0], s->host_stage[1]})
+  for (void* p : {(void*)s->A0, (void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0], s->host_stage[1]})
     if (p) cudaFree(p);
   if (s->loss_host) cudaFreeHost(s->loss_host);
   for (cudaEvent_t e : s->ev_grad) cudaEventDestroy(e);
@@ -649,8 +676,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   Feeds f;
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
   s->launches = s->gemm_launches = 0;
-  ST(run_forward(s, f, rows, st));
-  ST(run_loss(s, f, rows, st));
+  ST(run_forward(s, f, rows, st, FWD_TRAIN));
   ST(run_backward(s, rows, st, 0));
   CU(cudaGetLastError());
   s->last_launches = s->launches;
@@ -697,9 +723,10 @@ dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* fe
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
   if (fetch < 0 || fetch >= (int)s->remap.size() || !out) return fail(DFLOW_INVALID_ARGUMENT, "bad fetch");
   const int sid = s->remap[fetch];
-  ST(run_forward(s, f, rows, st));
+  if (sid == s->cost && s->loss_kind == DFLOW_LOSS_MSE && !f.y)
+    return fail(DFLOW_INVALID_ARGUMENT, "fetching the MSE cost needs y");
+  ST(run_forward(s, f, rows, st, FWD_ONLY));
   if (sid == s->cost) {
-    ST(run_loss(s, f, rows, st));
     CU(cudaMemcpyAsync(out, s->loss_dev, sizeof(float), cudaMemcpyDeviceToDevice, st));
     return DFLOW_OK;
   }
@@ -722,8 +749,7 @@ dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_
   Feeds f;
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
   if (n < 0 || (n > 0 && (!grads || !out))) return fail(DFLOW_INVALID_ARGUMENT, "bad fetch arrays");
-  ST(run_forward(s, f, rows, st));
-  ST(run_loss(s, f, rows, st));
+  ST(run_forward(s, f, rows, st, FWD_FETCH));
   ST(run_backward(s, rows, st, 1));
   for (int i = 0; i < n; ++i) {
     const int sid = (grads[i] >= 0 && grads[i] < (int)s->remap.size()) ? s->remap[grads[i]] : -1;

@@ -39,7 +39,8 @@ struct Layer {
   void* recv = nullptr;           // alltoall landing [Ppad] (u16 or f32)
   void* own = nullptr;            // owner's reduced shard [shard]
   void* gath = nullptr;           // allgather landing [Ppad]
-  GemmPlan fwd, dgrad, wgrad32, wgrad16;
+  float* colsum_ws = nullptr;     // fused db partials [ceil(cap/32), out]
+  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16;
   bool has_fwd = false, has_dgrad = false, has_wgrad16 = false;
 };
 
@@ -69,7 +70,6 @@ struct dflow_session {
   double* loss_partials = nullptr;
   float* loss_dev = nullptr;      // [2]: local C_r, reduced sum
   float* loss_host = nullptr;     // pinned
-  float* colsum_ws = nullptr;
   uint32_t* mask_dev = nullptr;
   int64_t mask_words_cap = 0;
   void* host_stage[2] = {nullptr, nullptr};  // device copies of host feeds (e2e path)
