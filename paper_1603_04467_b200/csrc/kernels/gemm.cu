@@ -79,6 +79,7 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi) {
   } else if (a_mn && b_mn) {
     if (epi == EPI_F32) return kernel_ptr<BN, CG, true, true, EPI_F32>();
     if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, true, true, EPI_TRUNC16>();
+    if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, true, true, EPI_SGD_APPLY>();
   }
   return nullptr;
 }
@@ -164,8 +165,9 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.denom_pow2 = (mn > 0 && (mn & (mn - 1)) == 0) ? 1 : 0;
   a.inv_denom = 1.0f / a.loss_denom;
   a.vec_y = aligned16(d.y, d.ldy, 4) ? 1 : 0;
-  a.group_m = 16;
-  if (const char* e = getenv("DFLOW_GEMM_GROUP")) a.group_m = atoi(e) > 0 ? atoi(e) : 16;
+  a.group_m = d.group > 0 ? d.group : 8;
+  if (const char* e = getenv("DFLOW_GEMM_GROUP")) a.group_m = atoi(e) > 0 ? atoi(e) : a.group_m;
+  a.sgd_lr = d.sgd_lr;
   a.sched = default_sched();
   if (!a.sched) {
     snprintf(g_err, sizeof g_err, "could not allocate the tile-scheduler counters");
@@ -175,6 +177,7 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.loss_partials = d.loss_partials;
   a.colsum_ws = d.colsum_ws;
   if ((d.epilogue == EPI_F32 && !d.out_f32) || (d.epilogue == EPI_TRUNC16 && !d.out) ||
+      (d.epilogue == EPI_SGD_APPLY && (!d.out_f32 || !d.out)) ||
       (d.epilogue == EPI_RELUGRAD && (!d.out || !d.mask)) ||
       (d.epilogue == EPI_BIAS_RELU && (!d.bias || (!d.out && !d.out_f32))) ||
       (d.epilogue == EPI_BIAS_RELU_LOSS && (!d.bias || !d.out || (d.loss_kind == 0 && !d.y)))) {

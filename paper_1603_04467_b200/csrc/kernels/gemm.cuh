@@ -291,6 +291,38 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = u32_as_f32(r[j]);
           }
+        } else if constexpr (EPI == EPI_SGD_APPLY) {
+          // N = 1: ApplyGradientDescent fused into the dW epilogue (a4 + a9):
+          // W <- fl(W - fl(lr * g)) on the fp32 master, bf16 working copy refreshed (RNE)
+          float* w = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
+          __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+          if (full_chunk && args.vec_out32 && args.vec_out) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              float4 w0 = *reinterpret_cast<const float4*>(w + j);
+              float4 w1 = *reinterpret_cast<const float4*>(w + j + 4);
+              w0.x = __fsub_rn(w0.x, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 0])));
+              w0.y = __fsub_rn(w0.y, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 1])));
+              w0.z = __fsub_rn(w0.z, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 2])));
+              w0.w = __fsub_rn(w0.w, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 3])));
+              w1.x = __fsub_rn(w1.x, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 4])));
+              w1.y = __fsub_rn(w1.y, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 5])));
+              w1.z = __fsub_rn(w1.z, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 6])));
+              w1.w = __fsub_rn(w1.w, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 7])));
+              *reinterpret_cast<float4*>(w + j) = w0;
+              *reinterpret_cast<float4*>(w + j + 4) = w1;
+              *reinterpret_cast<uint4*>(wb + j) = make_uint4(pack_bf16x2(w0.x, w0.y), pack_bf16x2(w0.z, w0.w),
+                                                             pack_bf16x2(w1.x, w1.y), pack_bf16x2(w1.z, w1.w));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (gn + j < args.N) {
+                const float nw = __fsub_rn(w[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
+                w[j] = nw;
+                wb[j] = __float2bfloat16_rn(nw);
+              }
+          }
         } else if constexpr (EPI == EPI_TRUNC16) {
           uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
           if (full_chunk && args.vec_out) {

@@ -11,6 +11,7 @@ enum GemmEpilogue : int {
   EPI_TRUNC16 = 1,    // out_u16[m,n] = bits(acc) >> 16              (a4 + a6 fused)
   EPI_BIAS_RELU = 2,  // a = relu(acc + bias[n]); out_bf16 (RNE) and/or out_f32  (a1)
   EPI_RELUGRAD = 3,   // out_bf16 = acc * 1[mask_bf16[m,n] > 0]        (a3) [+ fused db partials]
+  EPI_SGD_APPLY = 5,  // out_f32 (fp32 master W) -= lr * acc; out (bf16 copy) = RNE(W)   (a4 + a9, N = 1)
   EPI_BIAS_RELU_LOSS = 4,  // a = relu(acc + bias) [-> out_f32]; loss seed dz -> out_bf16 (a1 + a2)
                            // [+ fused db partials, + loss partials]
 };
@@ -40,6 +41,7 @@ struct GemmArgs {
   int group_m;            // tile raster: M-tiles per group (L2 reuse of the B panels)
   int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
   float seed_const;       // 1 / rows (SUM seed)
+  float sgd_lr;           // EPI_SGD_APPLY learning rate
   double* loss_partials;  // [grid * 4] per-(CTA, epilogue warp) partial sums
   // EPI_RELUGRAD / EPI_BIAS_RELU_LOSS: column sums of the stored dz per 32-row block
   float* colsum_ws;       // [ceil(M / 32), N] or nullptr
@@ -58,7 +60,9 @@ struct GemmDesc {
   int loss_kind;
   double* loss_partials;
   float* colsum_ws;                         // fused db partials (RELUGRAD, BIAS_RELU_LOSS)
-  int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair), 3 = 128x256 (1 CTA)
+  float sgd_lr;                             // EPI_SGD_APPLY
+  int group;       // tile-raster group (M tiles); 0 = default
+  int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)
 };
 

@@ -345,6 +345,16 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     w.out_f32 = ly.g32; w.ldo32 = ly.out;
     w.max_ctas = max_ctas;
     ST(gemm_plan(s, w, &ly.wgrad32));
+    if (s->opt.world == 1 && s->trainable) {
+      // no channel (reading A6): ApplyGradientDescent fused into the dW epilogue
+      GemmDesc wa = w;
+      wa.epilogue = EPI_SGD_APPLY;
+      wa.out_f32 = ly.W32; wa.ldo32 = ly.out;
+      wa.out = ly.Wbf; wa.ldo = ly.ld_wb;
+      wa.sgd_lr = ly.n.lr_W;
+      ST(gemm_plan(s, wa, &ly.wgrad_apply));
+      ly.has_wgrad_apply = true;
+    }
     if (s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
       w.epilogue = EPI_TRUNC16;
       w.out_f32 = nullptr;
@@ -517,12 +527,14 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
     tend(s, t, cs);
   }
   const int t = tbegin(s, 1, cs);
-  cudaError_t e = launch_apply_sgd(ly.W32, g32, g16, ly.in, ly.out, ly.Wbf, ly.ld_wb, ly.n.lr_W, cs);
+  const bool w_done = (N == 1 && ly.has_wgrad_apply);  // W already updated by the dW epilogue
+  cudaError_t e = w_done ? cudaSuccess
+                         : launch_apply_sgd(ly.W32, g32, g16, ly.in, ly.out, ly.Wbf, ly.ld_wb, ly.n.lr_W, cs);
   if (e == cudaSuccess)
     e = launch_apply_sgd(ly.b32, g32 ? g32 + nW : nullptr, g16 ? g16 + nW : nullptr, 1, ly.out, nullptr, 0,
                          ly.n.lr_b, cs);
   tend(s, t, cs);
-  ST(check_launch(s, e, 2, "apply"));
+  ST(check_launch(s, e, w_done ? 1 : 2, "apply"));
   if (N > 1) CU(cudaEventRecord(s->ev_apply[l], cs));
   return DFLOW_OK;
 }
@@ -533,7 +545,7 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
   for (int l = s->L - 1; l >= 0; --l) {
     Layer& ly = s->layers[l];
     if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
-    ST(launch_gemm(s, t16 ? ly.wgrad16 : ly.wgrad32, st));
+    ST(launch_gemm(s, t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32), st));
     // db_l: the producing epilogue left per-32-row column partials; sum them in order
     const int t = tbegin(s, 1, st);
     cudaError_t e = launch_colsum_final(ly.colsum_ws, static_cast<int>((rows + 31) / 32), ly.out,

@@ -40,8 +40,8 @@ struct Layer {
   void* own = nullptr;            // owner's reduced shard [shard]
   void* gath = nullptr;           // allgather landing [Ppad]
   float* colsum_ws = nullptr;     // fused db partials [ceil(cap/32), out]
-  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16;
-  bool has_fwd = false, has_dgrad = false, has_wgrad16 = false;
+  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16, wgrad_apply;
+  bool has_fwd = false, has_dgrad = false, has_wgrad16 = false, has_wgrad_apply = false;
 };
 
 struct TimedRange {
