@@ -210,6 +210,16 @@ dflow_status dflow_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int
                              int64_t ldo32, const float* bias, const void* mask, int64_t ldm, int tile,
                              void* stream);
 
+/* One 3xTF32 GEMM (fp32-faithful path, reading A14): every fp32 operand X is
+ * passed as the pair (X_hi = tf32_rna(X), X_lo = X - X_hi), same layout and
+ * leading dim (% 4 == 0); out_f32 = A_hi B_lo + A_lo B_hi + A_hi B_hi (fp32
+ * accumulate).  Majors and tiles as dflow_gemm_bf16; epilogue fp32 store only. */
+dflow_status dflow_gemm_3xtf32(int64_t M, int64_t N, int64_t K, const float* A_hi, const float* A_lo, int64_t lda,
+                               int a_mn, const float* B_hi, const float* B_lo, int64_t ldb, int b_mn, float* out_f32,
+                               int64_t ldo32, int tile, void* stream);
+/* The tf32 split itself (NK13, 3xTF32 path): hi = tf32_rna(src), lo = src - hi, n elements. */
+dflow_status dflow_split_tf32(const float* src, float* hi, float* lo, size_t n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

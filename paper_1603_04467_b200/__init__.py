@@ -93,6 +93,8 @@ _SIGS = {
     "dflow_exchange": (_i32, [_p, _p, _p, _sz, _p]),
     "dflow_gemm_bf16": (_i32, [_i64, _i64, _i64, _p, _i64, _i32, _p, _i64, _i32, _i32, _p, _i64, _p, _i64, _p, _p,
                                _i64, _i32, _p]),
+    "dflow_gemm_3xtf32": (_i32, [_i64, _i64, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i32, _p, _i64, _i32, _p]),
+    "dflow_split_tf32": (_i32, [_p, _p, _p, _sz, _p]),
 }
 
 for _name, (_res, _args) in _SIGS.items():

@@ -354,4 +354,37 @@ dflow_status dflow_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int
   GUARD_END
 }
 
+dflow_status dflow_gemm_3xtf32(int64_t M, int64_t N, int64_t K, const float* A_hi, const float* A_lo, int64_t lda,
+                               int a_mn, const float* B_hi, const float* B_lo, int64_t ldb, int b_mn, float* out_f32,
+                               int64_t ldo32, int tile, void* stream) {
+  GUARD_BEGIN
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(DFLOW_CUDA, "no CUDA device");
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  dflow::GemmDesc d{};
+  d.tf32 = true;
+  d.M = M; d.N = N; d.K = K;
+  d.A = A_hi; d.A2 = A_lo; d.lda = lda; d.a_mn = a_mn != 0;
+  d.B = B_hi; d.B2 = B_lo; d.ldb = ldb; d.b_mn = b_mn != 0;
+  d.epilogue = dflow::EPI_F32;
+  d.out_f32 = out_f32; d.ldo32 = ldo32;
+  d.tile = tile;
+  dflow::GemmPlan p;
+  cudaError_t e = dflow::gemm_prepare(d, sms, &p);
+  if (e != cudaSuccess) return fail(DFLOW_INVALID_ARGUMENT, "%s", dflow::gemm_last_error());
+  e = dflow::gemm_launch(p, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(DFLOW_CUDA, "%s", dflow::gemm_last_error());
+  return DFLOW_OK;
+  GUARD_END
+}
+
+dflow_status dflow_split_tf32(const float* src, float* hi, float* lo, size_t n, void* stream) {
+  if (n && (!src || !hi || !lo)) return fail(DFLOW_INVALID_ARGUMENT, "NULL pointer");
+  cudaError_t e = dflow::launch_split_tf32(src, 0, hi, lo, 0, 1, static_cast<int64_t>(n),
+                                           static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(DFLOW_CUDA, "split_tf32: %s", cudaGetErrorString(e));
+  return DFLOW_OK;
+}
+
 }  // extern "C"

@@ -95,6 +95,46 @@ __global__ void k_cast_bf16(const float* __restrict__ src, int64_t lds, __nv_bfl
   }
 }
 
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__global__ void k_split_tf32(const float* __restrict__ src, int64_t lds, float* __restrict__ hi,
+                             float* __restrict__ lo, int64_t ldd, int64_t rows, int64_t cols, int vec) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (vec) {  // cols % 4 == 0, aligned rows
+    const int64_t per_row = cols / 4, total = rows * per_row;
+    for (int64_t i = tid; i < total; i += stride) {
+      const int64_t r = i / per_row, c = (i - r * per_row) * 4;
+      const float4 a = *reinterpret_cast<const float4*>(src + r * lds + c);
+      const float4 b = make_float4(tf32_rna(a.x), tf32_rna(a.y), tf32_rna(a.z), tf32_rna(a.w));
+      *reinterpret_cast<float4*>(hi + r * ldd + c) = b;
+      *reinterpret_cast<float4*>(lo + r * ldd + c) =
+          make_float4(__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z), __fsub_rn(a.w, b.w));
+    }
+  } else {
+    for (int64_t i = tid; i < rows * cols; i += stride) {
+      const int64_t r = i / cols, c = i - r * cols;
+      const float a = src[r * lds + c], b = tf32_rna(a);
+      hi[r * ldd + c] = b;
+      lo[r * ldd + c] = __fsub_rn(a, b);
+    }
+  }
+}
+
+__global__ void k_join_tf32(const float* __restrict__ hi, const float* __restrict__ lo, int64_t ld, int64_t rows,
+                            int64_t cols, float* __restrict__ out) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < rows * cols; i += stride) {
+    const int64_t r = i / cols, c = i - r * cols;
+    out[i] = __fadd_rn(hi[r * ld + c], lo[r * ld + c]);
+  }
+}
+
 __global__ void k_copy_bf16(const __nv_bfloat16* __restrict__ src, int64_t lds, __nv_bfloat16* __restrict__ dst,
                             int64_t ldd, int64_t rows, int64_t cols) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -270,6 +310,25 @@ __global__ void k_apply_sgd(float* __restrict__ W, const float* __restrict__ g32
   }
 }
 
+__global__ void k_apply_sgd_tf32(float* __restrict__ W, const float* __restrict__ g32,
+                                 const uint16_t* __restrict__ g16, int64_t rows, int64_t cols,
+                                 float* __restrict__ whi, float* __restrict__ wlo, int64_t ldw, float lr) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n = rows * cols;
+  for (int64_t i = tid; i < n; i += stride) {
+    const float g = g16 ? __uint_as_float(static_cast<uint32_t>(g16[i]) << 16) : g32[i];
+    const float w = sgd(W[i], lr, g);
+    W[i] = w;
+    if (whi) {
+      const int64_t r = i / cols, c = i - r * cols;
+      const float b = tf32_rna(w);
+      whi[r * ldw + c] = b;
+      wlo[r * ldw + c] = __fsub_rn(w, b);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ masks
 template <typename T>
 __global__ void k_relu_mask_bits(const T* __restrict__ a, int64_t ld, int64_t rows, int64_t cols,
@@ -315,6 +374,30 @@ cudaError_t launch_cast_bf16(const float* src, int64_t lds, __nv_bfloat16* dst, 
   const int vec = (cols % 8 == 0) && (lds % 4 == 0) && (ldd % 8 == 0) && al16(src) && al16(dst);
   k_cast_bf16<<<blocks_for(vec ? rows * cols / 8 : rows * cols), kThreads, 0, s>>>(src, lds, dst, ldd, rows, cols,
                                                                                   vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_split_tf32(const float* src, int64_t lds, float* hi, float* lo, int64_t ldd, int64_t rows,
+                              int64_t cols, cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  const int vec = (cols % 4 == 0) && (lds % 4 == 0) && (ldd % 4 == 0) && al16(src) && al16(hi) && al16(lo);
+  k_split_tf32<<<blocks_for(vec ? rows * cols / 4 : rows * cols), kThreads, 0, s>>>(src, lds, hi, lo, ldd, rows,
+                                                                                     cols, vec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_join_tf32(const float* hi, const float* lo, int64_t ld, int64_t rows, int64_t cols, float* out,
+                             cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  k_join_tf32<<<blocks_for(rows * cols), kThreads, 0, s>>>(hi, lo, ld, rows, cols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_sgd_tf32(float* W, const float* g32, const uint16_t* g16, int64_t rows, int64_t cols,
+                                  float* whi, float* wlo, int64_t ldw, float lr, cudaStream_t s) {
+  const int64_t n = rows * cols;
+  if (n == 0) return cudaSuccess;
+  k_apply_sgd_tf32<<<blocks_for(n), kThreads, 0, s>>>(W, g32, g16, rows, cols, whi, wlo, ldw, lr);
   return cudaGetLastError();
 }
 

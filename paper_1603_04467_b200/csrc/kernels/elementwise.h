@@ -14,6 +14,13 @@ cudaError_t launch_expand16(const uint16_t* src, float* dst, size_t n, cudaStrea
 // NK13: dst bf16 [rows, ldd] = RNE(src f32 [rows, lds]) for cols columns.
 cudaError_t launch_cast_bf16(const float* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
                              int64_t cols, cudaStream_t s);
+// NK13 (3xTF32): hi = tf32_rna(x), lo = fl32(x - hi) for fp32 x [rows, lds] -> hi, lo [rows, ldd]
+// (reading A14).  hi + lo == x exactly.
+cudaError_t launch_split_tf32(const float* src, int64_t lds, float* hi, float* lo, int64_t ldd, int64_t rows,
+                              int64_t cols, cudaStream_t s);
+// dense fp32 [rows, cols] = hi + lo (exact reconstruction of a 3xTF32 operand pair)
+cudaError_t launch_join_tf32(const float* hi, const float* lo, int64_t ld, int64_t rows, int64_t cols, float* out,
+                             cudaStream_t s);
 // bf16 [rows, lds] -> bf16 [rows, ldd] (bf16 feeds with a foreign leading dim).
 cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat16* dst, int64_t ldd, int64_t rows,
                              int64_t cols, cudaStream_t s);
@@ -40,6 +47,9 @@ cudaError_t launch_scale_f32(float* x, int64_t n, float scale, cudaStream_t s);
 // W dense [n = rows*cols]; optional bf16 working copy wbf [rows, ldwb].
 cudaError_t launch_apply_sgd(float* W, const float* g32, const uint16_t* g16, int64_t rows, int64_t cols,
                              __nv_bfloat16* wbf, int64_t ldwb, float lr, cudaStream_t s);
+// Same update, refreshing the 3xTF32 operand pair (whi, wlo) [rows, ldw] instead.
+cudaError_t launch_apply_sgd_tf32(float* W, const float* g32, const uint16_t* g16, int64_t rows, int64_t cols,
+                                  float* whi, float* wlo, int64_t ldw, float lr, cudaStream_t s);
 
 // Bit-pack 1[a > 0] of a bf16 [rows, ld] activation (cols columns) row-major.
 cudaError_t launch_relu_mask_bits(const __nv_bfloat16* a, int64_t ld, int64_t rows, int64_t cols, uint32_t* bits,

@@ -1,4 +1,4 @@
-// Host launcher for the tcgen05 GEMM family (NK1-NK3): TMA descriptor
+// Host launcher for the tcgen05 GEMM family (NK1-NK6): TMA descriptor
 // encoding, tile-config choice, persistent grid sizing, cluster launch.
 #include <cudaTypedefs.h>
 
@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "gemm.cuh"
 #include "gemm.h"
@@ -28,26 +29,29 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map over a row-major matrix with `inner` contiguous elements
-// per row (logical extent), `outer` rows, row pitch `ld` elements.
-static bool make_tmap_bf16(CUtensorMap* m, const void* base, int64_t inner, int64_t outer, int64_t ld,
-                           uint32_t box_inner, uint32_t box_outer) {
+// 2-D tensor map (bf16 or fp32 elements) over a row-major matrix with `inner`
+// contiguous elements per row (logical extent), `outer` rows, pitch `ld` elements,
+// 128-byte swizzle, OOB zero fill.
+static bool make_tmap(CUtensorMap* m, const void* base, bool f32, int64_t inner, int64_t outer, int64_t ld,
+                      uint32_t box_inner, uint32_t box_outer, bool atom32 = false) {
   auto fn = encode_fn();
   if (!fn) {
     snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled unavailable");
     return false;
   }
-  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 2) & 15)) {
-    snprintf(g_err, sizeof g_err, "TMA needs 16-byte aligned base and row pitch (ld=%lld)", (long long)ld);
+  const int e = f32 ? 4 : 2;
+  if (!base || (reinterpret_cast<uintptr_t>(base) & 15) || ((ld * e) & 15)) {
+    snprintf(g_err, sizeof g_err, "TMA needs a 16-byte aligned base and row pitch (ld=%lld)", (long long)ld);
     return false;
   }
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * e)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%u,%u",
              (int)r, (long long)inner, (long long)outer, (long long)ld, box_inner, box_outer);
@@ -56,30 +60,31 @@ static bool make_tmap_bf16(CUtensorMap* m, const void* base, int64_t inner, int6
   return true;
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
+template <int BN, int CG, bool TF32, bool A_MN, bool B_MN, int EPI>
 static void* kernel_ptr() {
-  auto k = &gemm_bf16_kernel<BN, CG, A_MN, B_MN, EPI>;
+  auto k = &gemm_kernel<BN, CG, TF32, A_MN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, CG>::SMEM_BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, CG, TF32>::SMEM_BYTES);
     attr_set = true;
   }
   return reinterpret_cast<void*>(k);
 }
 
-template <int BN, int CG>
+// The (operand majors, epilogue) combinations the MLP step uses, per tile config.
+template <int BN, int CG, bool TF32>
 static void* select_kernel(bool a_mn, bool b_mn, int epi) {
-  if (!a_mn && b_mn) {
-    if (epi == EPI_BIAS_RELU) return kernel_ptr<BN, CG, false, true, EPI_BIAS_RELU>();
-    if (epi == EPI_F32) return kernel_ptr<BN, CG, false, true, EPI_F32>();
-    if (epi == EPI_BIAS_RELU_LOSS) return kernel_ptr<BN, CG, false, true, EPI_BIAS_RELU_LOSS>();
-  } else if (!a_mn && !b_mn) {
-    if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, false, false, EPI_RELUGRAD>();
-    if (epi == EPI_F32) return kernel_ptr<BN, CG, false, false, EPI_F32>();
-  } else if (a_mn && b_mn) {
-    if (epi == EPI_F32) return kernel_ptr<BN, CG, true, true, EPI_F32>();
-    if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, true, true, EPI_TRUNC16>();
-    if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, true, true, EPI_SGD_APPLY>();
+  if (!a_mn && b_mn) {  // forward: A K-major, W MN-major
+    if (epi == EPI_BIAS_RELU) return kernel_ptr<BN, CG, TF32, false, true, EPI_BIAS_RELU>();
+    if (epi == EPI_BIAS_RELU_LOSS) return kernel_ptr<BN, CG, TF32, false, true, EPI_BIAS_RELU_LOSS>();
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, true, EPI_F32>();
+  } else if (!a_mn && !b_mn) {  // dgrad: dZ K-major, W K-major
+    if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, TF32, false, false, EPI_RELUGRAD>();
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, false, EPI_F32>();
+  } else if (a_mn && b_mn) {  // wgrad: activations and dZ both MN-major
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, true, true, EPI_F32>();
+    if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16>();
+    if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, TF32, true, true, EPI_SGD_APPLY>();
   }
   return nullptr;
 }
@@ -116,28 +121,47 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
     const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
     tile = (pair_tiles >= num_sms / 2) ? 2 : 1;
   }
-  const int BN = (tile == 2) ? 256 : 128;
+  const bool tf = d.tf32;
+  // 3xTF32 pairs use N = 128 so the epilogue can hold a row's fp32 K-chunk sums in registers
+  const int BN = (tile == 2 && !tf) ? 256 : 128;
   const int CG = (tile == 2) ? 2 : 1;
   const int BN_CTA = BN / CG;
+  const int BK = tf ? 32 : 64;
+  const int CHUNK = BK;  // MN elements per 128-byte row (= BK for both element sizes)
   plan->d = d;
   plan->tile = tile;
   plan->cluster = CG;
   plan->tiles_m = static_cast<int>((d.M + 128 * CG - 1) / (128 * CG));
   plan->tiles_n = static_cast<int>((d.N + BN - 1) / BN);
-  void* k = (tile == 2) ? select_kernel<256, 2>(d.a_mn, d.b_mn, d.epilogue)
-                        : select_kernel<128, 1>(d.a_mn, d.b_mn, d.epilogue);
+  void* k = nullptr;
+  if (tile == 2)
+    k = tf ? select_kernel<128, 2, true>(d.a_mn, d.b_mn, d.epilogue) : select_kernel<256, 2, false>(d.a_mn, d.b_mn, d.epilogue);
+  else
+    k = tf ? select_kernel<128, 1, true>(d.a_mn, d.b_mn, d.epilogue) : select_kernel<128, 1, false>(d.a_mn, d.b_mn, d.epilogue);
   if (!k) {
     snprintf(g_err, sizeof g_err, "unsupported GEMM layout/epilogue (a_mn=%d b_mn=%d epi=%d)", d.a_mn, d.b_mn,
              d.epilogue);
     return cudaErrorInvalidValue;
   }
   plan->kernel = k;
-  plan->smem = (tile == 2) ? GemmCfg<256, 2>::SMEM_BYTES : GemmCfg<128, 1>::SMEM_BYTES;
+  plan->smem = (tile == 2) ? (tf ? GemmCfg<128, 2, true>::SMEM_BYTES : GemmCfg<256, 2, false>::SMEM_BYTES)
+                           : (tf ? GemmCfg<128, 1, true>::SMEM_BYTES : GemmCfg<128, 1, false>::SMEM_BYTES);
   const int64_t K = d.K > 0 ? d.K : 1;
-  bool ok = d.a_mn ? make_tmap_bf16(&plan->tmA, d.A, d.M, K, d.lda, 64, 64)
-                   : make_tmap_bf16(&plan->tmA, d.A, K, d.M, d.lda, 64, 128);
-  ok = ok && (d.b_mn ? make_tmap_bf16(&plan->tmB, d.B, d.N, K, d.ldb, 64, 64)
-                     : make_tmap_bf16(&plan->tmB, d.B, K, d.N, d.ldb, 64, BN_CTA));
+  // MN-major fp32 (tf32) operands: 32-byte-atom 128B swizzle (the UMMA SWIZZLE_128B_BASE32B layout)
+  auto map_a = [&](CUtensorMap* m, const void* p) {
+    return d.a_mn ? make_tmap(m, p, tf, d.M, K, d.lda, CHUNK, BK, tf) : make_tmap(m, p, tf, K, d.M, d.lda, BK, 128);
+  };
+  auto map_b = [&](CUtensorMap* m, const void* p) {
+    return d.b_mn ? make_tmap(m, p, tf, d.N, K, d.ldb, CHUNK, BK, tf)
+                  : make_tmap(m, p, tf, K, d.N, d.ldb, BK, BN_CTA);
+  };
+  bool ok = map_a(&plan->tmA, d.A) && map_b(&plan->tmB, d.B);
+  if (ok && tf) {
+    ok = map_a(&plan->tmA2, d.A2) && map_b(&plan->tmB2, d.B2);
+  } else if (ok) {
+    plan->tmA2 = plan->tmA;
+    plan->tmB2 = plan->tmB;
+  }
   if (!ok) return cudaErrorInvalidValue;
   GemmArgs& a = plan->args;
   memset(&a, 0, sizeof a);
@@ -147,16 +171,18 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.tiles_m = plan->tiles_m;
   a.tiles_n = plan->tiles_n;
   a.out = d.out;
+  a.out2 = d.out2;
   a.ldo = d.ldo;
   a.out_f32 = d.out_f32;
   a.ldo32 = d.ldo32;
   a.bias = d.bias;
   a.mask = d.mask;
   a.ldm = d.ldm;
-  const int out_elem = (d.epilogue == EPI_F32) ? 4 : 2;
-  a.vec_out = aligned16(d.out, d.ldo, out_elem) ? 1 : 0;
+  const int op_elem = tf ? 4 : 2;
+  const int out_elem = (d.epilogue == EPI_TRUNC16) ? 2 : op_elem;
+  a.vec_out = aligned16(d.out, d.ldo, out_elem) && (!tf || d.epilogue == EPI_TRUNC16 || aligned16(d.out2, d.ldo, 4)) ? 1 : 0;
   a.vec_out32 = aligned16(d.out_f32, d.ldo32, 4) ? 1 : 0;
-  a.vec_mask = aligned16(d.mask, d.ldm, 2) ? 1 : 0;
+  a.vec_mask = aligned16(d.mask, d.ldm, op_elem) ? 1 : 0;
   a.y = d.y;
   a.ldy = d.ldy;
   a.loss_kind = d.loss_kind;
@@ -176,15 +202,17 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.seed_const = 1.0f / static_cast<float>(d.M);
   a.loss_partials = d.loss_partials;
   a.colsum_ws = d.colsum_ws;
+  const bool need_lo = tf && d.epilogue != EPI_F32 && d.epilogue != EPI_TRUNC16;
   if ((d.epilogue == EPI_F32 && !d.out_f32) || (d.epilogue == EPI_TRUNC16 && !d.out) ||
       (d.epilogue == EPI_SGD_APPLY && (!d.out_f32 || !d.out)) ||
       (d.epilogue == EPI_RELUGRAD && (!d.out || !d.mask)) ||
       (d.epilogue == EPI_BIAS_RELU && (!d.bias || (!d.out && !d.out_f32))) ||
-      (d.epilogue == EPI_BIAS_RELU_LOSS && (!d.bias || !d.out || (d.loss_kind == 0 && !d.y)))) {
+      (d.epilogue == EPI_BIAS_RELU_LOSS && (!d.bias || !d.out || (d.loss_kind == 0 && !d.y))) ||
+      (need_lo && d.out && !d.out2)) {
     snprintf(g_err, sizeof g_err, "missing GEMM epilogue operand (epi=%d)", d.epilogue);
     return cudaErrorInvalidValue;
   }
-  int clusters = (num_sms - (d.max_ctas > 0 ? 0 : 0)) / CG;
+  int clusters = num_sms / CG;
   if (d.max_ctas > 0 && d.max_ctas < num_sms) clusters = d.max_ctas / CG;
   const int tiles = plan->tiles_m * plan->tiles_n;
   if (clusters > tiles) clusters = tiles;
@@ -207,7 +235,8 @@ cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  void* args[3] = {const_cast<CUtensorMap*>(&plan.tmA), const_cast<CUtensorMap*>(&plan.tmB),
+  void* args[5] = {const_cast<CUtensorMap*>(&plan.tmA), const_cast<CUtensorMap*>(&plan.tmB),
+                   const_cast<CUtensorMap*>(&plan.tmA2), const_cast<CUtensorMap*>(&plan.tmB2),
                    const_cast<GemmArgs*>(&plan.args)};
   cudaError_t e = cudaLaunchKernelExC(&cfg, plan.kernel, args);
   if (e != cudaSuccess) snprintf(g_err, sizeof g_err, "GEMM launch failed: %s", cudaGetErrorString(e));

@@ -1,7 +1,10 @@
-// NK1-NK3: persistent, warp-specialised tcgen05 GEMM for sm_100a with fused
-// epilogues (BiasAdd+Relu, ReluGrad, fp32 store, 32->16 truncation).
+// NK1-NK6: persistent, warp-specialised tcgen05 GEMM for sm_100a with fused
+// epilogues (BiasAdd+Relu, loss seed, ReluGrad, db column sums, fp32 store,
+// 32->16 truncation, SGD update), in two precisions:
 //
-//   C[m, n] = sum_k A(m, k) * B(k, n)        bf16 operands, fp32 accumulate in TMEM
+//   bf16   C = A B                  kind::f16, bf16 operands (RNE), fp32 accumulate in TMEM
+//   3xTF32 C = Ab Bs + As Bb + Ab Bb kind::tf32, every fp32 operand X stored as the pair
+//          (Xb = tf32_rna(X), Xs = X - Xb) (reading A14); the two small products first
 //
 // Operand majors (what the MLP step needs):
 //   forward  A_{l-1}[b,in]  (K-major)   x  W_l[in,out]      (MN-major B)
@@ -9,43 +12,53 @@
 //   wgrad    A_{l-1}[b,in]  (MN-major)  x  dZ_l[b,out]      (MN-major B)
 //
 // Roles (256 threads): warp 0 = TMA producer, warp 1 = MMA issuer (leader CTA
-// only), warp 2 = TMEM allocator, warps 4..7 = epilogue (TMEM lane quarters
-// 0..3).  Pipelines: smem stages full/empty (TMA <-> MMA), a double-buffered
-// TMEM accumulator full/empty (MMA <-> epilogue), and a static persistent tile
-// schedule (grid = #SMs / CG clusters, M-grouped tile order for L2 reuse).
+// only), warp 2 = TMEM allocator, warp 3 = tile scheduler (leader CTA), warps
+// 4..7 = epilogue (TMEM lane quarters 0..3).  Pipelines: smem stages full/empty
+// (TMA <-> MMA), a double-buffered TMEM accumulator full/empty (MMA <->
+// epilogue), and a 2-deep tile-id ring fed by a global atomic counter (dynamic
+// persistent schedule over an M-grouped raster, for L2 reuse).
 // CG = 2 runs cta_group::2: an MMA of M = 256 spans a CTA pair; each CTA loads
 // half of A (its 128 rows) and half of B (BN/2 columns); completions are
 // signalled on the leader's barriers; commits multicast to both CTAs.
 //
-// Shared-memory tiles use the 128-byte swizzle (1024-byte atoms of 8 x 128 B):
-//   K-major  tile [rows][64 k]            : SBO = 1024 B, k-step of 16 = +32 B
-//   MN-major tile [mn/64][64 k][64 mn]    : LBO = 8192 B (next 64-wide MN chunk),
-//                                           SBO = 1024 B (next 8 k-rows), k-step = +2048 B
+// Shared-memory tiles use the 128-byte swizzle (1024-byte atoms of 8 x 128 B);
+// E = element bytes (2 bf16, 4 fp32/tf32), BK = 128/E, K_MMA = 32/E:
+//   K-major  tile [rows][BK]                 : SBO = 1024 B, k-step = +32 B
+//   MN-major tile [mn/(128/E)][BK][128/E]    : LBO = BK*128 B (next MN chunk),
+//                                              SBO = 1024 B (next 8 k-rows), k-step = +K_MMA*128 B
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "gemm.h"
 #include "ptx.cuh"
 
 namespace dflow {
 
-template <int BN, int CG>
+template <int BN, int CG, bool TF32>
 struct GemmCfg {
-  static constexpr int BM = 128;                 // rows per CTA
-  static constexpr int BK = 64;                  // 64 bf16 = one 128-byte swizzle row
-  static constexpr int BN_CTA = BN / CG;         // B columns loaded by each CTA
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN_CTA * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int E = TF32 ? 4 : 2;          // operand element bytes
+  static constexpr int BM = 128;                  // rows per CTA
+  static constexpr int BK = 128 / E;              // one 128-byte swizzle row of K
+  static constexpr int KMMA = 32 / E;             // K per tcgen05.mma
+  static constexpr int CHUNK = 128 / E;           // MN elements per 128-byte MN-major row
+  static constexpr int NOPS = TF32 ? 2 : 1;       // operand parts (big, small)
+  static constexpr int BN_CTA = BN / CG;          // B columns loaded by each CTA
+  static constexpr int A_TILE = BM * BK * E;      // 16 KB
+  static constexpr int B_TILE = BN_CTA * BK * E;  // 16 KB (BN_CTA = 128)
+  static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;       // two accumulator buffers
+  static constexpr int TMEM_COLS = 2 * BN;        // two accumulator buffers
   static constexpr int BAR_BYTES = (2 * STAGES + 8) * 8 + 32;
-  static constexpr int SCHED_CONSUMERS = (CG == 2) ? 11 : 6;  // producer x CG + MMA + 4 epilogue warps x CG
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + alignment slack
+  static constexpr int SCHED_CONSUMERS = (CG == 2) ? 11 : 6;  // producer x CG + MMA + 4 epilogue warps x CG
+  // k-blocks per TMEM accumulation chunk: 3xTF32 flushes every 128 of K into fp32
+  // registers (reading A25); bf16 accumulates the whole K in TMEM
+  static constexpr int KB_PER_CHUNK = TF32 ? 4 : (1 << 30);
   static_assert(TMEM_COLS >= 32 && TMEM_COLS <= 512 && (TMEM_COLS & (TMEM_COLS - 1)) == 0, "tmem cols");
-  static_assert(BN % 32 == 0 && BN_CTA % 64 == 0, "tile N");
+  static_assert(BN % 32 == 0 && BN_CTA % CHUNK == 0, "tile N");
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int group, int& tm, int& tn) {
@@ -65,13 +78,72 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-template <int BN, int CG, bool A_MN, bool B_MN, int EPI>
+// tf32 round-to-nearest (ties away), returned in an fp32 container (low 13 bits 0)
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Store 32 consecutive operand values of one row: bf16 (RNE) or the 3xTF32 pair.
+// Returns (in v) the value the next GEMM will see for each element: bf16-rounded
+// value, or the exact fp32 value (= big + small) in the 3xTF32 path.
+template <bool TF32>
+__device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, void* lo_base, int64_t ld, int64_t gm,
+                                              int gn, int N, bool vec) {
+  const bool full = gn + 32 <= N;
+  if constexpr (!TF32) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+    __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(hi_base) + gm * ld + gn;
+    if (full && vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 8)
+        *reinterpret_cast<uint4*>(o + j) = make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                                                      pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (gn + j < N) o[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else {
+    float* oh = reinterpret_cast<float*>(hi_base) + gm * ld + gn;
+    float* ol = reinterpret_cast<float*>(lo_base) + gm * ld + gn;
+    if (full && vec) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        float b[4], s[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          b[e] = tf32_rna(v[j + e]);
+          s[e] = __fsub_rn(v[j + e], b[e]);
+        }
+        *reinterpret_cast<float4*>(oh + j) = make_float4(b[0], b[1], b[2], b[3]);
+        *reinterpret_cast<float4*>(ol + j) = make_float4(s[0], s[1], s[2], s[3]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (gn + j < N) {
+          const float b = tf32_rna(v[j]);
+          oh[j] = b;
+          ol[j] = __fsub_rn(v[j], b);
+        }
+    }
+  }
+}
+
+template <int BN, int CG, bool TF32, bool A_MN, bool B_MN, int EPI>
 __global__ void __launch_bounds__(256, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const GemmArgs args) {
-  using Cfg = GemmCfg<BN, CG>;
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
+                const GemmArgs args) {
+  using Cfg = GemmCfg<BN, CG, TF32>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, BN_CTA = Cfg::BN_CTA, STAGES = Cfg::STAGES;
-  constexpr int A_BYTES = Cfg::A_BYTES, STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int A_TILE = Cfg::A_TILE, B_TILE = Cfg::B_TILE, STAGE_BYTES = Cfg::STAGE_BYTES;
+  constexpr int CHUNK = Cfg::CHUNK, KMMA = Cfg::KMMA, NOPS = Cfg::NOPS;
+  constexpr int CHUNK_BYTES = BK * 128;  // one MN-major chunk: BK k-rows of 128 bytes
+  using OpT = typename std::conditional<TF32, float, __nv_bfloat16>::type;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* tiles = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -115,6 +187,10 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if constexpr (TF32) {
+      ptx::prefetch_tmap(&tmA2);
+      ptx::prefetch_tmap(&tmB2);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -155,24 +231,30 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb = full0 + stage * 8;
           if (cta_rank == 0) ptx::mbar_arrive_expect_tx(ptx::smem_u32(&full[stage]), CG * STAGE_BYTES);
-          const uint32_t sa = ptx::smem_u32(tiles + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t s0 = ptx::smem_u32(tiles + stage * STAGE_BYTES);
           const int k0 = kb * BK;
 #pragma unroll
-          for (int i = 0; i < (A_MN ? BM / 64 : 1); ++i) {
-            const uint32_t dst = sa + i * (64 * BK * 2);
-            const int c0 = A_MN ? (m0 + 64 * i) : k0;
-            const int c1 = A_MN ? k0 : m0;
-            if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, &tmA, fb, c0, c1);
-            else ptx::tma_load_2d(dst, &tmA, fb, c0, c1);
-          }
+          for (int part = 0; part < NOPS; ++part) {
+            const CUtensorMap* ma = part ? &tmA2 : &tmA;
+            const CUtensorMap* mb = part ? &tmB2 : &tmB;
+            const uint32_t sa = s0 + part * A_TILE;
+            const uint32_t sb = s0 + NOPS * A_TILE + part * B_TILE;
 #pragma unroll
-          for (int i = 0; i < (B_MN ? BN_CTA / 64 : 1); ++i) {
-            const uint32_t dst = sb + i * (64 * BK * 2);
-            const int c0 = B_MN ? (n0 + 64 * i) : k0;
-            const int c1 = B_MN ? k0 : n0;
-            if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, &tmB, fb, c0, c1);
-            else ptx::tma_load_2d(dst, &tmB, fb, c0, c1);
+            for (int i = 0; i < (A_MN ? BM / CHUNK : 1); ++i) {
+              const uint32_t dst = sa + i * CHUNK_BYTES;
+              const int c0 = A_MN ? (m0 + CHUNK * i) : k0;
+              const int c1 = A_MN ? k0 : m0;
+              if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, ma, fb, c0, c1);
+              else ptx::tma_load_2d(dst, ma, fb, c0, c1);
+            }
+#pragma unroll
+            for (int i = 0; i < (B_MN ? BN_CTA / CHUNK : 1); ++i) {
+              const uint32_t dst = sb + i * CHUNK_BYTES;
+              const int c0 = B_MN ? (n0 + CHUNK * i) : k0;
+              const int c1 = B_MN ? k0 : n0;
+              if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, mb, fb, c0, c1);
+              else ptx::tma_load_2d(dst, mb, fb, c0, c1);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -181,7 +263,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (one thread of the leader CTA) =====================
     if (cta_rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc(BM * CG, BN, A_MN, B_MN, false);
+      constexpr uint32_t idesc = ptx::make_idesc(BM * CG, BN, A_MN, B_MN, TF32);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -192,28 +274,56 @@ __global__ void __launch_bounds__(256, 1)
         const int t = next_tile(sslot, sph, false);
         if (t >= num_tiles) break;
         if (num_kb == 0) continue;
-        ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1);
-        ptx::tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+        // K is processed in chunks, each accumulated from zero into one of the two TMEM
+        // buffers (bf16: one chunk per tile; 3xTF32: 128-wide K chunks summed in fp32 by the
+        // epilogue, because the tensor core truncates when it accumulates, reading A25)
+        uint32_t d = 0;
         for (int kb = 0; kb < num_kb; ++kb) {
+          const bool chunk_start = (kb % Cfg::KB_PER_CHUNK) == 0;
+          const bool chunk_end = (kb % Cfg::KB_PER_CHUNK) == Cfg::KB_PER_CHUNK - 1 || kb == num_kb - 1;
+          if (chunk_start) {
+            ptx::mbar_wait(ptx::smem_u32(&tempty[acc]), acc_phase ^ 1);
+            ptx::tc_fence_after();
+            d = tmem_base + acc * BN;
+          }
           ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
           ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(tiles + stage * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t s0 = ptx::smem_u32(tiles + stage * STAGE_BYTES);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t adesc = A_MN ? ptx::smem_desc_sw128(sa + k * 2048, 64 * BK * 2, 1024)
-                                        : ptx::smem_desc_sw128(sa + k * 32, 16, 1024);
-            const uint64_t bdesc = B_MN ? ptx::smem_desc_sw128(sb + k * 2048, 64 * BK * 2, 1024)
-                                        : ptx::smem_desc_sw128(sb + k * 32, 16, 1024);
-            ptx::mma_ss<CG, false>(d, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < BK / KMMA; ++k) {
+            const uint32_t ka = A_MN ? k * KMMA * 128 : k * 32;
+            const uint32_t kbo = B_MN ? k * KMMA * 128 : k * 32;
+            // MN-major tf32 operands use the 32-byte-atom 128B swizzle (4-row period, SBO = 4 rows)
+            auto mn_desc = [&](uint32_t addr) {
+              return TF32 ? ptx::smem_desc_sw128_base32(addr, CHUNK_BYTES, 512)
+                          : ptx::smem_desc_sw128(addr, CHUNK_BYTES, 1024);
+            };
+            auto adesc = [&](int part) {
+              const uint32_t a = s0 + part * A_TILE + ka;
+              return A_MN ? mn_desc(a) : ptx::smem_desc_sw128(a, 16, 1024);
+            };
+            auto bdesc = [&](int part) {
+              const uint32_t b = s0 + NOPS * A_TILE + part * B_TILE + kbo;
+              return B_MN ? mn_desc(b) : ptx::smem_desc_sw128(b, 16, 1024);
+            };
+            const uint32_t first = (chunk_start && k == 0) ? 0u : 1u;
+            if constexpr (TF32) {
+              // small products first (reading A14), then big * big
+              ptx::mma_ss<CG, true>(d, adesc(0), bdesc(1), idesc, first);
+              ptx::mma_ss<CG, true>(d, adesc(1), bdesc(0), idesc, 1u);
+              ptx::mma_ss<CG, true>(d, adesc(0), bdesc(0), idesc, 1u);
+            } else {
+              ptx::mma_ss<CG, false>(d, adesc(0), bdesc(0), idesc, first);
+            }
           }
           ptx::mma_commit<CG>(ptx::smem_u32(&empty[stage]), 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (chunk_end) {
+            ptx::mma_commit<CG>(ptx::smem_u32(&tfull[acc]), 0x3);
+            acc ^= 1;
+            if (acc == 0) acc_phase ^= 1;
+          }
         }
-        ptx::mma_commit<CG>(ptx::smem_u32(&tfull[acc]), 0x3);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
       }
     }
   } else if (warp == 3) {
@@ -264,142 +374,166 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
       const int gm = tm * (BM * CG) + cta_rank * BM + q * 32 + lane;
       const bool row_ok = gm < args.M;
-      if (num_kb > 0) {
+      const uint32_t tmem_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+      auto release_tmem = [&]() {  // hand the TMEM buffer back to the MMA warp
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+          else ptx::mbar_arrive(ptx::smem_u32(&tempty[acc]));
+        }
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      };
+      // 3xTF32: the K chunks arrive one TMEM buffer at a time; sum them in fp32 (RN)
+      float kacc[TF32 ? BN : 1];
+      if constexpr (TF32) {
+        const int nchunks = (num_kb + Cfg::KB_PER_CHUNK - 1) / Cfg::KB_PER_CHUNK;
+#pragma unroll
+        for (int j = 0; j < BN; ++j) kacc[j] = 0.f;
+        for (int ch = 0; ch < nchunks; ++ch) {
+          ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            ptx::tmem_ld_32x32b_x32(tmem_row + acc * BN + c * 32, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) kacc[c * 32 + j] = __fadd_rn(kacc[c * 32 + j], u32_as_f32(r[j]));
+          }
+          release_tmem();
+        }
+      } else if (num_kb > 0) {
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
         ptx::tc_fence_after();
       }
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      auto column_chunk = [&](int c, uint32_t (&r)[32]) {
         const int gn = tn * BN + c * 32;
-        uint32_t r[32];
-        if (num_kb > 0) {
-          ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
-          ptx::tmem_ld_wait();
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;  // K == 0: the empty sum
-        }
-        if (row_ok && gn < args.N) {
+        const bool active = row_ok && gn < args.N;
         const bool full_chunk = gn + 32 <= args.N;
         if constexpr (EPI == EPI_F32) {
-          float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
-          if (full_chunk && args.vec_out32) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<uint4*>(o + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = u32_as_f32(r[j]);
-          }
-        } else if constexpr (EPI == EPI_SGD_APPLY) {
-          // N = 1: ApplyGradientDescent fused into the dW epilogue (a4 + a9):
-          // W <- fl(W - fl(lr * g)) on the fp32 master, bf16 working copy refreshed (RNE)
-          float* w = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
-          __nv_bfloat16* wb = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
-          if (full_chunk && args.vec_out32 && args.vec_out) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              float4 w0 = *reinterpret_cast<const float4*>(w + j);
-              float4 w1 = *reinterpret_cast<const float4*>(w + j + 4);
-              w0.x = __fsub_rn(w0.x, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 0])));
-              w0.y = __fsub_rn(w0.y, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 1])));
-              w0.z = __fsub_rn(w0.z, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 2])));
-              w0.w = __fsub_rn(w0.w, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 3])));
-              w1.x = __fsub_rn(w1.x, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 4])));
-              w1.y = __fsub_rn(w1.y, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 5])));
-              w1.z = __fsub_rn(w1.z, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 6])));
-              w1.w = __fsub_rn(w1.w, __fmul_rn(args.sgd_lr, u32_as_f32(r[j + 7])));
-              *reinterpret_cast<float4*>(w + j) = w0;
-              *reinterpret_cast<float4*>(w + j + 4) = w1;
-              *reinterpret_cast<uint4*>(wb + j) = make_uint4(pack_bf16x2(w0.x, w0.y), pack_bf16x2(w0.z, w0.w),
-                                                             pack_bf16x2(w1.x, w1.y), pack_bf16x2(w1.z, w1.w));
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (gn + j < args.N) {
-                const float nw = __fsub_rn(w[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
-                w[j] = nw;
-                wb[j] = __float2bfloat16_rn(nw);
-              }
-          }
-        } else if constexpr (EPI == EPI_TRUNC16) {
-          uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
-          if (full_chunk && args.vec_out) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 v;
-              v.x = (r[j] >> 16) | (r[j + 1] & 0xFFFF0000u);
-              v.y = (r[j + 2] >> 16) | (r[j + 3] & 0xFFFF0000u);
-              v.z = (r[j + 4] >> 16) | (r[j + 5] & 0xFFFF0000u);
-              v.w = (r[j + 6] >> 16) | (r[j + 7] & 0xFFFF0000u);
-              *reinterpret_cast<uint4*>(o + j) = v;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = static_cast<uint16_t>(r[j] >> 16);
-          }
-        } else if constexpr (EPI == EPI_BIAS_RELU) {
-          float v[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float bj = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
-            const float z = __fadd_rn(u32_as_f32(r[j]), bj);
-            v[j] = (z < 0.f) ? 0.f : z;  // Relu; NaN propagates (non-finite guard)
-          }
-          if (args.out != nullptr) {
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
-            if (full_chunk && args.vec_out) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8)
-                *reinterpret_cast<uint4*>(o + j) =
-                    make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
-                               pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
-            } else {
-  #pragma unroll
-              for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = __float2bfloat16_rn(v[j]);
-            }
-          }
-          if (args.out_f32 != nullptr) {
+          if (active) {
             float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
             if (full_chunk && args.vec_out32) {
 #pragma unroll
-              for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<uint4*>(o + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
             } else {
-  #pragma unroll
-              for (int j = 0; j < 32; ++j) if (gn + j < args.N) o[j] = v[j];
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (gn + j < args.N) o[j] = u32_as_f32(r[j]);
             }
           }
-        }
-        }  // row_ok && gn < N
-        if constexpr (EPI == EPI_RELUGRAD || EPI == EPI_BIAS_RELU_LOSS) {
-          // dz values as stored (bf16-rounded), 0 outside the matrix; fused column sums.
+        } else if constexpr (EPI == EPI_TRUNC16) {
+          if (active) {
+            uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+            if (full_chunk && args.vec_out) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 v;
+                v.x = (r[j] >> 16) | (r[j + 1] & 0xFFFF0000u);
+                v.y = (r[j + 2] >> 16) | (r[j + 3] & 0xFFFF0000u);
+                v.z = (r[j + 4] >> 16) | (r[j + 5] & 0xFFFF0000u);
+                v.w = (r[j + 6] >> 16) | (r[j + 7] & 0xFFFF0000u);
+                *reinterpret_cast<uint4*>(o + j) = v;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (gn + j < args.N) o[j] = static_cast<uint16_t>(r[j] >> 16);
+            }
+          }
+        } else if constexpr (EPI == EPI_SGD_APPLY) {
+          // N = 1: ApplyGradientDescent fused into the dW epilogue (a4 + a9):
+          // W <- fl(W - fl(lr * g)) on the fp32 master; the operand copy (bf16 RNE or
+          // the tf32 pair) is refreshed from the new W
+          if (active) {
+            float* w = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
+            float v[32];
+            if (full_chunk && args.vec_out32) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(w + j);
+                v[j] = w4.x; v[j + 1] = w4.y; v[j + 2] = w4.z; v[j + 3] = w4.w;
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __fsub_rn(v[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
+#pragma unroll
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4*>(w + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                v[j] = 0.f;
+                if (gn + j < args.N) {
+                  v[j] = __fsub_rn(w[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
+                  w[j] = v[j];
+                }
+              }
+            }
+            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0);
+          }
+        } else if constexpr (EPI == EPI_BIAS_RELU) {
+          if (active) {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float bj = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
+              const float z = __fadd_rn(u32_as_f32(r[j]), bj);
+              v[j] = (z < 0.f) ? 0.f : z;  // Relu; NaN propagates (non-finite guard)
+            }
+            if (args.out_f32 != nullptr) {
+              float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
+              if (full_chunk && args.vec_out32) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (gn + j < args.N) o[j] = v[j];
+              }
+            }
+            if (args.out != nullptr)
+              store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0);
+          }
+        } else if constexpr (EPI == EPI_RELUGRAD || EPI == EPI_BIAS_RELU_LOSS) {
+          // dz values as stored, 0 outside the matrix; fused db column sums.
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
-          if (row_ok && gn < args.N) {
-            const bool full_chunk = gn + 32 <= args.N;
-            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+          if (active) {
             if constexpr (EPI == EPI_RELUGRAD) {
-              const __nv_bfloat16* mrow =
-                  reinterpret_cast<const __nv_bfloat16*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
+              const OpT* mrow = reinterpret_cast<const OpT*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
               if (full_chunk && args.vec_mask) {
+                if constexpr (!TF32) {
 #pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                  const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j));
-                  const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+                  for (int j = 0; j < 32; j += 8) {
+                    const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j));
+                    const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) {
-                    const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
-                    // bf16 > 0  <=>  sign bit clear, not +0, not NaN
-                    const bool pos = (h & 0x8000u) == 0 && h != 0 && h <= 0x7F80u;
-                    v[j + e] = pos ? u32_as_f32(r[j + e]) : 0.f;
+                    for (int e = 0; e < 8; ++e) {
+                      const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
+                      // bf16 > 0  <=>  sign bit clear, not +0, not NaN
+                      const bool pos = (h & 0x8000u) == 0 && h != 0 && h <= 0x7F80u;
+                      v[j + e] = pos ? u32_as_f32(r[j + e]) : 0.f;
+                    }
+                  }
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 32; j += 4) {
+                    const float4 m4 = __ldg(reinterpret_cast<const float4*>(mrow + j));
+                    v[j] = m4.x > 0.f ? u32_as_f32(r[j]) : 0.f;
+                    v[j + 1] = m4.y > 0.f ? u32_as_f32(r[j + 1]) : 0.f;
+                    v[j + 2] = m4.z > 0.f ? u32_as_f32(r[j + 2]) : 0.f;
+                    v[j + 3] = m4.w > 0.f ? u32_as_f32(r[j + 3]) : 0.f;
                   }
                 }
               } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                  if (gn + j < args.N) v[j] = (__bfloat162float(mrow[j]) > 0.f) ? u32_as_f32(r[j]) : 0.f;
+                  if (gn + j < args.N) v[j] = (static_cast<float>(mrow[j]) > 0.f) ? u32_as_f32(r[j]) : 0.f;
               }
             } else {  // EPI_BIAS_RELU_LOSS: a = relu(acc + b); loss seed (reading A2, A10, A20)
               const float* yrow = args.y + static_cast<int64_t>(gm) * args.ldy + gn;
@@ -449,20 +583,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            // round to the stored bf16 and store
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
-            if (full_chunk && args.vec_out) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8)
-                *reinterpret_cast<uint4*>(o + j) =
-                    make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
-                               pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (gn + j < args.N) o[j] = __float2bfloat16_rn(v[j]);
-            }
+            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0);
           }
           if (args.colsum_ws != nullptr) {
             // transpose-reduce: after 5 butterfly steps lane l holds the sum over this
@@ -483,17 +604,30 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         __syncwarp();
-      }
-      if (num_kb > 0) {
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (CG == 2) ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
-          else ptx::mbar_arrive(ptx::smem_u32(&tempty[acc]));
+      };
+      if constexpr (TF32) {
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(kacc[c * 32 + j]);
+          column_chunk(c, r);
         }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN / 32; ++c) {
+          uint32_t r[32];
+          if (num_kb > 0) {
+            ptx::tmem_ld_32x32b_x32(tmem_row + acc * BN + c * 32, r);
+            ptx::tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = 0u;  // K == 0: the empty sum
+          }
+          column_chunk(c, r);
+        }
+        if (num_kb > 0) release_tmem();
       }
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
     }
     if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
 #pragma unroll

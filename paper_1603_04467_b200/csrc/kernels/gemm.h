@@ -1,4 +1,4 @@
-// Host-side GEMM launcher interface (NK1-NK3).  See gemm.cuh for the kernel.
+// Host-side GEMM launcher interface (NK1-NK6).  See gemm.cuh for the kernel.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -6,28 +6,31 @@
 
 namespace dflow {
 
+// "operand" outputs are written as bf16 (RNE) in the bf16 path, or as the tf32
+// pair (big -> out, small -> out2, fp32 each) in the 3xTF32 path.
 enum GemmEpilogue : int {
-  EPI_F32 = 0,        // out_f32[m,n] = acc
-  EPI_TRUNC16 = 1,    // out_u16[m,n] = bits(acc) >> 16              (a4 + a6 fused)
-  EPI_BIAS_RELU = 2,  // a = relu(acc + bias[n]); out_bf16 (RNE) and/or out_f32  (a1)
-  EPI_RELUGRAD = 3,   // out_bf16 = acc * 1[mask_bf16[m,n] > 0]        (a3) [+ fused db partials]
-  EPI_SGD_APPLY = 5,  // out_f32 (fp32 master W) -= lr * acc; out (bf16 copy) = RNE(W)   (a4 + a9, N = 1)
-  EPI_BIAS_RELU_LOSS = 4,  // a = relu(acc + bias) [-> out_f32]; loss seed dz -> out_bf16 (a1 + a2)
-                           // [+ fused db partials, + loss partials]
+  EPI_F32 = 0,             // out_f32[m,n] = acc                                           (a4 fetch, dx)
+  EPI_TRUNC16 = 1,         // out_u16[m,n] = bits(acc) >> 16                               (a4 + a6)
+  EPI_BIAS_RELU = 2,       // a = relu(acc + bias[n]) -> operand out and/or fp32 out_f32   (a1)
+  EPI_RELUGRAD = 3,        // dz = acc * 1[mask[m,n] > 0] -> operand out [+ db partials]    (a3 + a5)
+  EPI_BIAS_RELU_LOSS = 4,  // a = relu(acc + bias) [-> out_f32]; loss seed dz -> operand out
+                           // [+ db partials, + loss partials]                            (a1 + a2 + a5)
+  EPI_SGD_APPLY = 5,       // out_f32 (fp32 master W) -= lr * acc; operand copy refreshed  (a4 + a9, N = 1)
 };
 
 // Kernel arguments (by value, __grid_constant__-style).
 struct GemmArgs {
   int M, N, K;
   int tiles_m, tiles_n;   // tiles of (128*CG) x BN
-  void* out;              // bf16 (BIAS_RELU, RELUGRAD) or u16 (TRUNC16)
+  void* out;              // operand output (bf16 / tf32 big) or u16 (TRUNC16)
+  void* out2;             // 3xTF32: operand output small part
   int64_t ldo;
-  float* out_f32;         // fp32 output (F32, optional for BIAS_RELU)
+  float* out_f32;         // fp32 output (F32, SGD master, optional for BIAS_RELU[_LOSS])
   int64_t ldo32;
   const float* bias;      // [N]
-  const void* mask;       // RELUGRAD: the forward activation A_{l-1} (bf16)
+  const void* mask;       // RELUGRAD: the forward activation A_{l-1} (bf16, or tf32 big part)
   int64_t ldm;
-  int vec_out;            // 1: 16-byte vector stores are aligned for out
+  int vec_out;            // 1: 16-byte vector stores are aligned for out (and out2)
   int vec_out32;          // 1: 16-byte vector stores are aligned for out_f32
   int vec_mask;           // 1: 16-byte vector loads are aligned for mask
   // EPI_BIAS_RELU_LOSS
@@ -49,10 +52,11 @@ struct GemmArgs {
 
 struct GemmDesc {
   int64_t M, N, K;
-  const void* A;  int64_t lda; bool a_mn;   // a_mn=0: A(m,k)=A[m*lda+k]; 1: A(m,k)=A[k*lda+m]
-  const void* B;  int64_t ldb; bool b_mn;   // b_mn=0: B(k,n)=B[n*ldb+k]; 1: B(k,n)=B[k*ldb+n]
+  bool tf32;                                // false: bf16 operands; true: 3xTF32 (fp32 big/small pairs)
+  const void* A;  const void* A2; int64_t lda; bool a_mn;  // a_mn=0: A(m,k)=A[m*lda+k]; 1: A[k*lda+m]
+  const void* B;  const void* B2; int64_t ldb; bool b_mn;  // b_mn=0: B(k,n)=B[n*ldb+k]; 1: B[k*ldb+n]
   int epilogue;                             // GemmEpilogue
-  void* out;  int64_t ldo;
+  void* out;  void* out2; int64_t ldo;
   float* out_f32; int64_t ldo32;
   const float* bias;
   const void* mask; int64_t ldm;
@@ -68,7 +72,7 @@ struct GemmDesc {
 
 // Prepared launch: tensor maps + args, reusable across calls while buffers stay put.
 struct GemmPlan {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmA2, tmB2;
   GemmDesc d;
   GemmArgs args;
   int tile;

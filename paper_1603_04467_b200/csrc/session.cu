@@ -223,21 +223,52 @@ dflow_status dmalloc(dflow_session* s, T** p, size_t elems) {
   return DFLOW_OK;
 }
 
+// bf16 operand, or the fp32 (hi, lo) pair of the 3xTF32 path
+dflow_status alloc_operand(dflow_session* s, Operand* op, size_t elems) {
+  if (s->tf32) {
+    float *h, *l;
+    ST(dmalloc(s, &h, elems));
+    ST(dmalloc(s, &l, elems));
+    op->hi = h;
+    op->lo = l;
+  } else {
+    __nv_bfloat16* h;
+    ST(dmalloc(s, &h, elems));
+    op->hi = h;
+    op->lo = nullptr;
+  }
+  return DFLOW_OK;
+}
+
+void free_operand(Operand& op) {
+  if (op.hi) cudaFree(op.hi);
+  if (op.lo) cudaFree(op.lo);
+  op.hi = op.lo = nullptr;
+}
+
+// Refresh the operand copy of a fp32 matrix src [rows, lds] (RNE bf16 or the tf32 split).
+cudaError_t to_operand(dflow_session* s, const float* src, int64_t lds, const Operand& op, int64_t ldd, int64_t rows,
+                       int64_t cols, cudaStream_t st) {
+  if (s->tf32)
+    return launch_split_tf32(src, lds, static_cast<float*>(op.hi), static_cast<float*>(op.lo), ldd, rows, cols, st);
+  return launch_cast_bf16(src, lds, static_cast<__nv_bfloat16*>(op.hi), ldd, rows, cols, st);
+}
+
 dflow_status alloc_state(dflow_session* s) {
   const int N = s->opt.world;
   const int64_t cap = s->cap;
   s->ld_A0 = pad_to(s->layers[0].in, 8);
-  ST(dmalloc(s, &s->A0, cap * s->ld_A0));
+  ST(alloc_operand(s, &s->A0, cap * s->ld_A0));
   int64_t max_out = 0;
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     ly.ld_out = pad_to(ly.out, 8);
     ly.ld_wb = pad_to(ly.out, 8);
     ST(dmalloc(s, &ly.W32, ly.in * ly.out));
-    ST(dmalloc(s, &ly.Wbf, ly.in * ly.ld_wb));
+    ST(alloc_operand(s, &ly.Wop, ly.in * ly.ld_wb));
     ST(dmalloc(s, &ly.b32, ly.out));
-    if (l + 1 < s->L) ST(dmalloc(s, &ly.A, cap * ly.ld_out));
-    ST(dmalloc(s, &ly.dZ, cap * ly.ld_out));
+    if (l + 1 < s->L) ST(alloc_operand(s, &ly.A, cap * ly.ld_out));
+    ST(alloc_operand(s, &ly.dZ, cap * ly.ld_out));
     ly.P = ly.in * ly.out + ly.out;
     ly.Ppad = pad_to(ly.P, 8 * N);
     ly.shard = ly.Ppad / N;
@@ -290,25 +321,27 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
   const int max_ctas = (s->opt.world > 1 && s->opt.overlap && s->opt.sm_reserve > 0)
                            ? std::max(2, s->num_sms - s->opt.sm_reserve)
                            : 0;
+  const bool tf = s->tf32;
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     const bool last = (l + 1 == s->L);
-    const __nv_bfloat16* Aprev = (l == 0) ? s->A0 : s->layers[l - 1].A;
+    const Operand& Aprev = (l == 0) ? s->A0 : s->layers[l - 1].A;
     const int64_t ld_prev = (l == 0) ? s->ld_A0 : s->layers[l - 1].ld_out;
     GemmDesc f{};
+    f.tf32 = tf;
     f.M = rows; f.N = ly.out; f.K = ly.in;
-    f.A = Aprev; f.lda = ld_prev; f.a_mn = false;
-    f.B = ly.Wbf; f.ldb = ly.ld_wb; f.b_mn = true;
+    f.A = Aprev.hi; f.A2 = Aprev.lo; f.lda = ld_prev; f.a_mn = false;
+    f.B = ly.Wop.hi; f.B2 = ly.Wop.lo; f.ldb = ly.ld_wb; f.b_mn = true;
     f.bias = ly.b32;
     f.max_ctas = max_ctas;
     if (!last) {
       f.epilogue = EPI_BIAS_RELU;
-      f.out = ly.A; f.ldo = ly.ld_out;
+      f.out = ly.A.hi; f.out2 = ly.A.lo; f.ldo = ly.ld_out;
       ST(gemm_plan(s, f, &ly.fwd));
     } else {
       // last layer: Relu + loss seed + db partials fused (a1 + a2 + a5); y is patched per call
       f.epilogue = EPI_BIAS_RELU_LOSS;
-      f.out = ly.dZ; f.ldo = ly.ld_out;
+      f.out = ly.dZ.hi; f.out2 = ly.dZ.lo; f.ldo = ly.ld_out;
       f.loss_kind = s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1;
       f.y = s->AL32; f.ldy = s->ld_AL32;  // placeholder pointer, replaced at launch
       f.loss_partials = s->loss_partials;
@@ -319,6 +352,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       GemmDesc p = f;  // forward-only without a target: plain Relu, fp32 A_L
       p.epilogue = EPI_BIAS_RELU;
       p.out = nullptr;
+      p.out2 = nullptr;
       p.y = nullptr; p.loss_partials = nullptr; p.colsum_ws = nullptr;
       ST(gemm_plan(s, p, &ly.fwd_plain));
     }
@@ -326,21 +360,23 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     if (l > 0) {
       const Layer& lp = s->layers[l - 1];
       GemmDesc d{};
+      d.tf32 = tf;
       d.M = rows; d.N = ly.in; d.K = ly.out;
-      d.A = ly.dZ; d.lda = ly.ld_out; d.a_mn = false;
-      d.B = ly.Wbf; d.ldb = ly.ld_wb; d.b_mn = false;
+      d.A = ly.dZ.hi; d.A2 = ly.dZ.lo; d.lda = ly.ld_out; d.a_mn = false;
+      d.B = ly.Wop.hi; d.B2 = ly.Wop.lo; d.ldb = ly.ld_wb; d.b_mn = false;
       d.epilogue = EPI_RELUGRAD;
-      d.out = lp.dZ; d.ldo = lp.ld_out;
-      d.mask = lp.A; d.ldm = lp.ld_out;
+      d.out = lp.dZ.hi; d.out2 = lp.dZ.lo; d.ldo = lp.ld_out;
+      d.mask = lp.A.hi; d.ldm = lp.ld_out;
       d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
     }
     GemmDesc w{};
+    w.tf32 = tf;
     w.M = ly.in; w.N = ly.out; w.K = rows;
-    w.A = Aprev; w.lda = ld_prev; w.a_mn = true;
-    w.B = ly.dZ; w.ldb = ly.ld_out; w.b_mn = true;
+    w.A = Aprev.hi; w.A2 = Aprev.lo; w.lda = ld_prev; w.a_mn = true;
+    w.B = ly.dZ.hi; w.B2 = ly.dZ.lo; w.ldb = ly.ld_out; w.b_mn = true;
     w.epilogue = EPI_F32;
     w.out_f32 = ly.g32; w.ldo32 = ly.out;
     w.max_ctas = max_ctas;
@@ -350,7 +386,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       GemmDesc wa = w;
       wa.epilogue = EPI_SGD_APPLY;
       wa.out_f32 = ly.W32; wa.ldo32 = ly.out;
-      wa.out = ly.Wbf; wa.ldo = ly.ld_wb;
+      wa.out = ly.Wop.hi; wa.out2 = ly.Wop.lo; wa.ldo = ly.ld_wb;
       wa.sgd_lr = ly.n.lr_W;
       ST(gemm_plan(s, wa, &ly.wgrad_apply));
       ly.has_wgrad_apply = true;
@@ -358,7 +394,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     if (s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
       w.epilogue = EPI_TRUNC16;
       w.out_f32 = nullptr;
-      w.out = ly.q16; w.ldo = ly.out;
+      w.out = ly.q16; w.out2 = nullptr; w.ldo = ly.out;
       ST(gemm_plan(s, w, &ly.wgrad16));
       ly.has_wgrad16 = true;
     }
@@ -456,9 +492,9 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
   if (f.ldx < in) return fail(DFLOW_INVALID_ARGUMENT, "ld of x < its width");
   int t = tbegin(s, 1, st);
   cudaError_t e = (s->x_dtype == DFLOW_F32)
-                      ? launch_cast_bf16(static_cast<const float*>(f.x), f.ldx, s->A0, s->ld_A0, rows, in, st)
-                      : launch_copy_bf16(static_cast<const __nv_bfloat16*>(f.x), f.ldx, s->A0, s->ld_A0, rows, in,
-                                         st);
+                      ? to_operand(s, static_cast<const float*>(f.x), f.ldx, s->A0, s->ld_A0, rows, in, st)
+                      : launch_copy_bf16(static_cast<const __nv_bfloat16*>(f.x), f.ldx,
+                                         static_cast<__nv_bfloat16*>(s->A0.hi), s->ld_A0, rows, in, st);
   tend(s, t, st);
   ST(check_launch(s, e, 1, "input cast"));
   for (int l = 0; l + 1 < s->L; ++l) ST(launch_gemm(s, s->layers[l].fwd, st));
@@ -528,8 +564,12 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
   }
   const int t = tbegin(s, 1, cs);
   const bool w_done = (N == 1 && ly.has_wgrad_apply);  // W already updated by the dW epilogue
-  cudaError_t e = w_done ? cudaSuccess
-                         : launch_apply_sgd(ly.W32, g32, g16, ly.in, ly.out, ly.Wbf, ly.ld_wb, ly.n.lr_W, cs);
+  cudaError_t e = cudaSuccess;
+  if (!w_done)
+    e = s->tf32 ? launch_apply_sgd_tf32(ly.W32, g32, g16, ly.in, ly.out, static_cast<float*>(ly.Wop.hi),
+                                        static_cast<float*>(ly.Wop.lo), ly.ld_wb, ly.n.lr_W, cs)
+                : launch_apply_sgd(ly.W32, g32, g16, ly.in, ly.out, static_cast<__nv_bfloat16*>(ly.Wop.hi),
+                                   ly.ld_wb, ly.n.lr_W, cs);
   if (e == cudaSuccess)
     e = launch_apply_sgd(ly.b32, g32 ? g32 + nW : nullptr, g16 ? g16 + nW : nullptr, 1, ly.out, nullptr, 0,
                          ly.n.lr_b, cs);
@@ -612,8 +652,6 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     return fail(DFLOW_INVALID_ARGUMENT, "need 0 <= rank < world");
   if (opt.precision != DFLOW_PRECISION_BF16 && opt.precision != DFLOW_PRECISION_3XTF32)
     return fail(DFLOW_INVALID_ARGUMENT, "unknown precision");
-  if (opt.precision == DFLOW_PRECISION_3XTF32)
-    return fail(DFLOW_UNIMPLEMENTED, "the 3xTF32 path is not built yet (SURVEY.md §8 NK4-NK6)");
   if (opt.exchange < DFLOW_EXCHANGE_TRUNC16 || opt.exchange > DFLOW_EXCHANGE_NONE)
     return fail(DFLOW_INVALID_ARGUMENT, "unknown exchange mode");
   if (opt.max_local_rows <= 0) return fail(DFLOW_INVALID_ARGUMENT, "max_local_rows must be > 0");
@@ -621,8 +659,12 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   dflow_session* s = new dflow_session();
   s->opt = opt;
   s->cap = opt.max_local_rows;
+  s->tf32 = opt.precision == DFLOW_PRECISION_3XTF32;
+  s->esz = s->tf32 ? 4 : 2;
   dflow_status st = insert_exchange(user, opt.world, opt.exchange, &s->g, &s->remap);
   if (st == DFLOW_OK) st = match_graph(s);
+  if (st == DFLOW_OK && s->tf32 && s->x_dtype != DFLOW_F32)
+    st = fail(DFLOW_INVALID_ARGUMENT, "the 3xTF32 path needs an fp32 x placeholder");
   if (st != DFLOW_OK) {
     delete s;
     return st;
@@ -665,11 +707,15 @@ void session_destroy(dflow_session* s) {
   cudaDeviceSynchronize();
   if (s->nccl) ncclCommDestroy(s->nccl);
   for (Layer& ly : s->layers) {
-    for (void* p : {(void*)ly.W32, (void*)ly.Wbf, (void*)ly.b32, (void*)ly.A, (void*)ly.dZ, (void*)ly.g32,
-                    (void*)ly.q16, ly.recv, ly.own, ly.gath, (void*)ly.colsum_ws})
+    for (void* p : {(void*)ly.W32, (void*)ly.b32, (void*)ly.g32, (void*)ly.q16, ly.recv, ly.own, ly.gath,
+                    (void*)ly.colsum_ws})
       if (p) cudaFree(p);
+    free_operand(ly.Wop);
+    free_operand(ly.A);
+    free_operand(ly.dZ);
   }
-  for (void* p : {(void*)s->A0, (void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0], s->host_stage[1]})
+  free_operand(s->A0);
+  for (void* p : {(void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0], s->host_stage[1]})
     if (p) cudaFree(p);
   if (s->loss_host) cudaFreeHost(s->loss_host);
   for (cudaEvent_t e : s->ev_grad) cudaEventDestroy(e);
@@ -745,9 +791,15 @@ dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* fe
   for (int l = 0; l < s->L; ++l) {
     if (s->layers[l].n.relu != sid) continue;
     const Layer& ly = s->layers[l];
-    cudaError_t e = (l + 1 == s->L)
-                        ? launch_copy_f32(s->AL32, s->ld_AL32, rows, ly.out, static_cast<float*>(out), ly.out, st)
-                        : launch_bf16_to_f32(ly.A, ly.ld_out, rows, ly.out, static_cast<float*>(out), st);
+    cudaError_t e;
+    if (l + 1 == s->L)
+      e = launch_copy_f32(s->AL32, s->ld_AL32, rows, ly.out, static_cast<float*>(out), ly.out, st);
+    else if (s->tf32)
+      e = launch_join_tf32(static_cast<const float*>(ly.A.hi), static_cast<const float*>(ly.A.lo), ly.ld_out, rows,
+                           ly.out, static_cast<float*>(out), st);
+    else
+      e = launch_bf16_to_f32(static_cast<const __nv_bfloat16*>(ly.A.hi), ly.ld_out, rows, ly.out,
+                             static_cast<float*>(out), st);
     return check_launch(s, e, 1, "fetch copy");
   }
   return fail(DFLOW_UNIMPLEMENTED, "forward fetch must be a Relu node or the cost");
@@ -777,9 +829,10 @@ dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_
       } else if (sid == ly.n.dX && l == 0) {
         // dx = dZ_1 W_1^T (Fig.5), fp32, written straight by the GEMM epilogue
         GemmDesc d{};
+        d.tf32 = s->tf32;
         d.M = rows; d.N = ly.in; d.K = ly.out;
-        d.A = ly.dZ; d.lda = ly.ld_out; d.a_mn = false;
-        d.B = ly.Wbf; d.ldb = ly.ld_wb; d.b_mn = false;
+        d.A = ly.dZ.hi; d.A2 = ly.dZ.lo; d.lda = ly.ld_out; d.a_mn = false;
+        d.B = ly.Wop.hi; d.B2 = ly.Wop.lo; d.ldb = ly.ld_wb; d.b_mn = false;
         d.epilogue = EPI_F32;
         d.out_f32 = static_cast<float*>(out[i]); d.ldo32 = ly.in;
         GemmPlan p;
@@ -801,8 +854,13 @@ dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_hos
   const int64_t rows = s->last_rows;
   const int64_t words = (rows * ly.out + 31) / 32;
   cudaStream_t st = nullptr;
-  cudaError_t e = (layer == s->L) ? launch_relu_mask_bits_f32(s->AL32, s->ld_AL32, rows, ly.out, s->mask_dev, st)
-                                  : launch_relu_mask_bits(ly.A, ly.ld_out, rows, ly.out, s->mask_dev, st);
+  cudaError_t e;
+  if (layer == s->L)
+    e = launch_relu_mask_bits_f32(s->AL32, s->ld_AL32, rows, ly.out, s->mask_dev, st);
+  else if (s->tf32)  // mask from the tf32 big part (reading A24)
+    e = launch_relu_mask_bits_f32(static_cast<const float*>(ly.A.hi), ly.ld_out, rows, ly.out, s->mask_dev, st);
+  else
+    e = launch_relu_mask_bits(static_cast<const __nv_bfloat16*>(ly.A.hi), ly.ld_out, rows, ly.out, s->mask_dev, st);
   if (e != cudaSuccess) {
     s->poisoned = true;
     return fail(DFLOW_CUDA, "mask kernel: %s", cudaGetErrorString(e));
@@ -828,7 +886,7 @@ dflow_status session_variable_assign(dflow_session* s, dflow_node var, const voi
     CU(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
   }
   if (!is_bias) {
-    cudaError_t e = launch_cast_bf16(ly.W32, ly.out, ly.Wbf, ly.ld_wb, ly.in, ly.out, st);
+    cudaError_t e = to_operand(s, ly.W32, ly.out, ly.Wop, ly.ld_wb, ly.in, ly.out, st);
     if (e != cudaSuccess) {
       s->poisoned = true;
       return fail(DFLOW_CUDA, "weight cast: %s", cudaGetErrorString(e));

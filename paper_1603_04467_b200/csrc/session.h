@@ -22,16 +22,23 @@ struct LayerNodes {
   float lr_W = 0.f, lr_b = 0.f;
 };
 
+// A GEMM operand in HBM: bf16 path -> hi only (bf16); 3xTF32 path -> the pair
+// hi = tf32_rna(x), lo = x - hi (fp32 each), same layout (reading A14).
+struct Operand {
+  void* hi = nullptr;
+  void* lo = nullptr;
+};
+
 struct Layer {
   LayerNodes n;
   int64_t in = 0, out = 0;
-  int64_t ld_out = 0;             // padded leading dim (elements) of bf16 [rows, out] buffers
-  int64_t ld_wb = 0;              // padded leading dim of the bf16 weight copy [in, ld_wb]
+  int64_t ld_out = 0;             // padded leading dim (elements) of [rows, out] operand buffers
+  int64_t ld_wb = 0;              // padded leading dim of the weight operand copy [in, ld_wb]
   float* W32 = nullptr;           // fp32 master [in*out] dense
-  __nv_bfloat16* Wbf = nullptr;   // bf16 working copy [in, ld_wb]
+  Operand Wop;                    // operand copy of W [in, ld_wb]
   float* b32 = nullptr;           // fp32 [out]
-  __nv_bfloat16* A = nullptr;     // bf16 activation [cap, ld_out] (all layers; last for masks)
-  __nv_bfloat16* dZ = nullptr;    // bf16 [cap, ld_out]
+  Operand A;                      // activation [cap, ld_out] (layers 1..L-1)
+  Operand dZ;                     // [cap, ld_out]
   // gradient bucket [dW_l || db_l], padded to Ppad = roundup(P, 8N)
   int64_t P = 0, Ppad = 0, shard = 0;
   float* g32 = nullptr;           // fp32 gradient bucket [Ppad]
@@ -63,7 +70,9 @@ struct dflow_session {
   int64_t cap = 0;
   int num_sms = 148;
   int64_t planned_rows = -1;
-  __nv_bfloat16* A0 = nullptr;    // bf16 copy of the x feed [cap, ld_A0]
+  bool tf32 = false;              // DFLOW_PRECISION_3XTF32
+  int esz = 2;                    // operand element bytes (2 bf16, 4 fp32)
+  dflow::Operand A0;              // operand copy of the x feed [cap, ld_A0]
   int64_t ld_A0 = 0;
   float* AL32 = nullptr;          // fp32 last activation [cap, ld_AL32]
   int64_t ld_AL32 = 0;
