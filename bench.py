@@ -52,6 +52,35 @@ def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+# ---------------------------------------------------------------- distributed plumbing (host logic)
+def shard_rows(global_batch: int, world: int, rank: int):
+    """Rows [row0, row0 + b) of the global batch for this rank (reading A4); B % N must be 0."""
+    if global_batch % world:
+        raise ValueError(f"global batch {global_batch} must divide by the number of GPUs {world}")
+    b = global_batch // world
+    return rank * b, b
+
+
+def broadcast_bytes(payload, dist, device, n: int = 128) -> bytes:
+    """Rank 0's n-byte payload (the NCCL unique id) to every rank through torch.distributed."""
+    import torch
+    t = torch.zeros(n, dtype=torch.uint8, device=device)
+    if dist.get_rank() == 0:
+        t.copy_(torch.frombuffer(bytearray(payload), dtype=torch.uint8))
+    dist.broadcast(t, 0)
+    return bytes(t.cpu().numpy().tobytes())
+
+
+def max_over_ranks(v: float, dist, device) -> float:
+    """Job time = the slowest rank's device time."""
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------- clocks
 class Clocks:
     """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
@@ -160,9 +189,13 @@ def run_reference(args, w):
 def config_dict(w, args, world):
     return {"workload": w.name, "global_batch": w.batch, "layers": w.layers, "width": w.dims[1],
             "dims": list(w.dims), "loss": w.loss, "lr": w.lr, "exchange": args.exchange,
-            "parallelism": f"dp{world}", "precision": "bf16 operands, fp32 accumulate + master weights",
-            "l2": "no flush: every step streams inputs and activations far larger than the 126 MB L2 "
-                  "(X fp32 1 GiB, each activation 512 MiB at N=1)"}
+            "parallelism": f"dp{world}",
+            "precision": ("3xTF32 split fp32 operands (big, small), fp32 accumulate + master weights"
+                          if w.precision == "3xtf32" else "bf16 operands, fp32 accumulate + master weights"),
+            "l2": ("no flush: every step streams inputs and activations far larger than the 126 MB L2 "
+                   f"(X fp32 {w.batch // world * w.dims[0] * 4 / 2**20:.0f} MiB per rank)")
+            if w.batch // world * w.dims[0] * 4 > 126 * 2**20 else
+            "inputs fit in L2 and are not flushed between steps (latency-bound configuration)"}
 
 
 # ---------------------------------------------------------------- GPU leg
@@ -178,20 +211,16 @@ def run_gpu(args, w):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1603_04467_b200 as D
 
-    if w.batch % world:
-        raise SystemExit("global batch must divide by the number of GPUs")
-    b = w.batch // world
+    row0, b = shard_rows(w.batch, world, rank)
     # NCCL id from rank 0, broadcast through torch.distributed (plumbing only)
     nid = None
     if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nid = bytes(idt.cpu().numpy().tobytes())
+        nid = broadcast_bytes(D.nccl_unique_id() if rank == 0 else None, dist, "cuda")
+    tf32 = w.precision == "3xtf32"
     mlp = D.mlp_graph(w.dims, w.loss, w.lr)
     opts = D.make_options(world=world, rank=rank, device=local, exchange=args.exchange, max_local_rows=b,
-                          overlap=1, sm_reserve=args.sm_reserve)
+                          overlap=1, sm_reserve=args.sm_reserve,
+                          precision=D.DFLOW_PRECISION_3XTF32 if tf32 else D.DFLOW_PRECISION_BF16)
     s = D.session_create(mlp, opts, nid)
     Ws, bs = synth.init_params(w)
     stream = torch.cuda.current_stream()
@@ -201,7 +230,7 @@ def run_gpu(args, w):
     for nid_, bb in zip(mlp.biases, bs):
         D.check(D.dflow_variable_assign(s, nid_, bb.ctypes.data_as(C.c_void_p), 0, sp))
     del Ws, bs
-    X, Y = synth.batch(w, rows=b, row0=rank * b)
+    X, Y = synth.batch(w, rows=b, row0=row0)
     Xd = torch.from_numpy(X).cuda()
     Yd = torch.from_numpy(Y).cuda()
     feeds = D.node_array([mlp.x, mlp.y])
@@ -217,13 +246,6 @@ def run_gpu(args, w):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     first_loss = C.c_float(0)
     step(C.byref(first_loss))
     for _ in range(max(0, args.warmup - 1)):
@@ -238,7 +260,7 @@ def run_gpu(args, w):
     e1.record(stream)
     barrier()
     clk = clocks.stop()
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms = max_over_ranks(e0.elapsed_time(e1), dist, "cuda")
     st = D.dflow_stats()
     D.check(D.dflow_session_stats(s, C.byref(st)))
     launches = st.launches_per_step
@@ -266,12 +288,22 @@ def run_gpu(args, w):
     for _ in range(e2e_steps):
         D.check(D.dflow_train_step_host(s, 2, feeds, hptrs, lds, b, C.byref(hl), sp))
     barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, dist, "cuda")
 
     pk = peaks()
     step_flops = w.flops_per_example() * w.batch
     value = w.batch * args.steps / (ms / 1000.0)
-    achieved = flops_per_launch / (gemm_avg_ms / 1000.0) / 1e12
+    if tf32:
+        # the tensor pipe runs 3 TF32 products per fp32-equivalent FLOP; TF32 dense peak =
+        # 1/2 of bf16 (B200_PROFILING.md nominal ratio 1.1 / 2.25 PF) x the measured bf16 peak
+        mma_mult, peak_t, peak_b, kname = 3.0, 0.5 * pk["bf16_sustained"], 0.5 * pk["bf16_burst"], \
+            "gemm_kernel<3xTF32> (tcgen05 kind::tf32, NK4-NK6)"
+        peak_note = ", TF32 = 0.5 x measured sustained bf16 (nominal ratio); achieved counts the 3 TF32 products"
+    else:
+        mma_mult, peak_t, peak_b, kname = 1.0, pk["bf16_sustained"], pk["bf16_burst"], \
+            "gemm_kernel<bf16> (tcgen05 kind::f16, NK1-NK3)"
+        peak_note = ", sustained bf16 (kernel timed inside a long step)"
+    achieved = mma_mult * flops_per_launch / (gemm_avg_ms / 1000.0) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tp):
@@ -290,18 +322,17 @@ def run_gpu(args, w):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (3xTF32)" if tf32 else "bf16",
             "data": "synthetic (seeded, synth/; X,Y ~ U[0,1), He-uniform W)",
             "config": config_dict(w, args, world),
-            "pct_tensor_peak": {"step_tflops": step_flops / (ms / args.steps / 1000.0) / 1e12 / world,
-                                "per_gpu_frac_of_sustained": step_flops / (ms / args.steps / 1000.0) / 1e12 / world
-                                / pk["bf16_sustained"],
-                                "per_gpu_frac_of_burst": step_flops / (ms / args.steps / 1000.0) / 1e12 / world
-                                / pk["bf16_burst"]},
-            "roofline": {"kernel": "gemm_bf16_kernel (tcgen05 NK1-NK3)", "bound": "tensor", "achieved": achieved,
-                         "peak": pk["bf16_sustained"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sustained"],
-                         "traffic": traffic, "peak_source": pk["source"] + ", sustained bf16 (kernel timed inside "
-                                                                            "a long step)",
+            "pct_tensor_peak": {"step_tflops": mma_mult * step_flops / (ms / args.steps / 1000.0) / 1e12 / world,
+                                "per_gpu_frac_of_sustained": mma_mult * step_flops / (ms / args.steps / 1000.0)
+                                / 1e12 / world / peak_t,
+                                "per_gpu_frac_of_burst": mma_mult * step_flops / (ms / args.steps / 1000.0)
+                                / 1e12 / world / peak_b},
+            "roofline": {"kernel": kname, "bound": "tensor", "achieved": achieved,
+                         "peak": peak_t, "unit": "TFLOP/s", "frac": achieved / peak_t,
+                         "traffic": traffic, "peak_source": pk["source"] + peak_note,
                          "avg_launch_ms": gemm_avg_ms, "flops_per_launch": flops_per_launch,
                          "gemm_share_of_step": st.gemm_ms / max(1e-9, st.gemm_ms + st.other_ms + st.exchange_ms)},
             "cpu_baseline": cpu,
