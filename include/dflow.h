@@ -132,6 +132,9 @@ typedef struct {
   int32_t overlap;        /* 1: per-layer exchange on a comm stream overlapped with backward  */
   int32_t sm_reserve;     /* SMs left free by the GEMMs for concurrent NCCL kernels          */
   int64_t max_local_rows; /* capacity b_max of every activation buffer                        */
+  int32_t p2p;            /* TRUNC16, N > 1: 1 = fused NVLink exchange (the dW epilogue stores the
+                             truncated tiles into the owners' buffers through CUDA IPC peer
+                             pointers; owner fold + all-gather by peer stores); 0 = NCCL calls  */
 } dflow_options;
 
 /* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */

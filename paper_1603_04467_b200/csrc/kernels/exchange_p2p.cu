@@ -1,0 +1,138 @@
+// Fused NVLink gradient exchange kernels (see exchange_p2p.h).  Arithmetic is the
+// same as the NCCL path (k_owner_reduce_t16): rank-order fp32 fold of the
+// expanded values, x (1/N), truncate — so both paths give the same bits.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "exchange_p2p.h"
+
+namespace dflow {
+
+namespace {
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// thread 0 of the block spins until flags[0..n) >= epoch, then the block proceeds
+__device__ __forceinline__ void block_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < n; ++r)
+      while (static_cast<int32_t>(ld_acquire_sys(flags + r) - epoch) < 0) __nanosleep(64);
+  }
+  __syncthreads();
+}
+
+// Every thread fences its peer stores; the last block to finish raises `phase` flags
+// flags[j][phase][rank] = epoch on every rank j.
+__device__ __forceinline__ void grid_signal(const P2PLayer& p, int phase, uint32_t epoch) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(&p.done[phase], 1);
+    if (prev == static_cast<int>(gridDim.x) - 1) {
+      p.done[phase] = 0;
+      __threadfence_system();
+      for (int j = 0; j < p.world; ++j) st_release_sys(p.flags[j] + phase * kMaxRanks + p.rank, epoch);
+    }
+  }
+}
+
+__global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int64_t cols, int64_t base_idx,
+                                   const P2PLayer p, uint32_t epoch) {
+  __shared__ float sm[8][33];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32LL + cl;
+  float t = 0.f;
+  if (c < cols) {
+    int k = g;
+    for (; k + 24 < chunks; k += 32) {
+      const float a0 = ws[(int64_t)k * cols + c], a1 = ws[(int64_t)(k + 8) * cols + c];
+      const float a2 = ws[(int64_t)(k + 16) * cols + c], a3 = ws[(int64_t)(k + 24) * cols + c];
+      t = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(t, a0), a1), a2), a3);
+    }
+    for (; k < chunks; k += 8) t = __fadd_rn(t, ws[(int64_t)k * cols + c]);
+  }
+  sm[g][cl] = t;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float s = sm[0][cl];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
+    const int64_t idx = base_idx + c;
+    const int owner = static_cast<int>(idx / p.shard);
+    p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
+        static_cast<uint16_t>(__float_as_uint(s) >> 16);
+  }
+  grid_signal(p, 0, epoch);
+}
+
+__global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch) {
+  block_wait_flags(p.flags[p.rank], p.world, epoch);  // every rank's contribution has landed
+  const float inv = 1.0f / static_cast<float>(p.world);
+  const uint16_t* recv = p.recv[p.rank];
+  const int64_t nv = p.shard / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += stride) {
+    float s[8];
+    {
+      const uint4 q = reinterpret_cast<const uint4*>(recv)[i];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16);
+    }
+    for (int r = 1; r < p.world; ++r) {  // left fold in rank order (reading A7)
+      const uint4 q = reinterpret_cast<const uint4*>(recv + r * p.shard)[i];
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16));
+    }
+    uint32_t o[4];
+#pragma unroll
+    for (int e = 0; e < 8; e += 2) {
+      const uint32_t lo = __float_as_uint(__fmul_rn(s[e], inv)) >> 16;
+      const uint32_t hi = __float_as_uint(__fmul_rn(s[e + 1], inv)) & 0xFFFF0000u;
+      o[e >> 1] = lo | hi;
+    }
+    const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+    for (int j = 0; j < p.world; ++j)  // all-gather leg: push q_bar to every rank (NVLink stores)
+      reinterpret_cast<uint4*>(p.gath[j] + static_cast<int64_t>(p.rank) * p.shard)[i] = ov;
+  }
+  grid_signal(p, 1, epoch);
+}
+
+__global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
+  block_wait_flags(flags, n, epoch);
+  __threadfence_system();
+}
+
+}  // namespace
+
+cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
+                                    uint32_t epoch, cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 31) / 32));
+  k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s) {
+  const int64_t nv = p.shard / 8;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((nv + 255) / 256, 148 * 2)));
+  k_owner_reduce_p2p<<<blocks, 256, 0, s>>>(p, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s) {
+  k_wait_flags<<<1, 32, 0, s>>>(flags, world, epoch);
+  return cudaGetLastError();
+}
+
+}  // namespace dflow

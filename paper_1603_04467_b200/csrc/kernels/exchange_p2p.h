@@ -1,0 +1,41 @@
+// Fused NVLink gradient exchange: the TRUNC16 schedule of
+// a6-a9 with peer-memory stores instead of NCCL calls.
+//
+//   wgrad GEMM (EPI_TRUNC16_P2P) : each rank stores bits(dW)>>16 straight into the
+//                                  owner's receive slot  recv[owner][rank*shard + i]
+//   colsum_final_p2p             : db the same way, then raises phase-0 flags on every
+//                                  owner: "rank r's layer-l contribution is complete"
+//   owner_reduce_p2p             : waits for all N phase-0 flags, folds its shard in rank
+//                                  order (x 1/N, truncate), stores q_bar into every
+//                                  rank's gath[rank*shard + i], raises phase-1 flags
+//   apply (+ wait)               : waits for all N phase-1 flags, applies expand(q_bar)
+//
+// Flags are monotonically increasing step epochs (no resets); ordering uses
+// system-scope fences and release/acquire flag accesses.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "gemm.h"
+
+namespace dflow {
+
+struct P2PLayer {
+  uint16_t* recv[kMaxRanks];   // rank j's receive area of this layer  [world * shard]
+  uint16_t* gath[kMaxRanks];   // rank j's gathered bucket             [world * shard]
+  uint32_t* flags[kMaxRanks];  // rank j's flags of this layer         [2][kMaxRanks]
+  int* done;                   // local grid-completion counters       [2]
+  int64_t shard;
+  int rank, world;
+};
+
+// db_l (sum of the per-32-row partials), truncated and stored at bucket index
+// base_idx + c in its owner's receive slot; then phase-0 flags.
+cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
+                                    uint32_t epoch, cudaStream_t s);
+// Owner step over peer memory (see above).
+cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s);
+// Block until all `world` phase-1 flags of this rank reach `epoch` (one CTA, acquire.sys).
+cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
+
+}  // namespace dflow

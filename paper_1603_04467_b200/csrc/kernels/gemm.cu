@@ -85,6 +85,7 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi) {
     if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, true, true, EPI_F32>();
     if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16>();
     if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, TF32, true, true, EPI_SGD_APPLY>();
+    if (epi == EPI_TRUNC16_P2P) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16_P2P>();
   }
   return nullptr;
 }
@@ -202,6 +203,17 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.seed_const = 1.0f / static_cast<float>(d.M);
   a.loss_partials = d.loss_partials;
   a.colsum_ws = d.colsum_ws;
+  if (d.epilogue == EPI_TRUNC16_P2P) {
+    if (!d.p2p_recv || d.p2p_world < 1 || d.p2p_world > kMaxRanks || d.p2p_shard <= 0 || d.p2p_shard % 8 ||
+        d.p2p_rank < 0 || d.p2p_rank >= d.p2p_world) {
+      snprintf(g_err, sizeof g_err, "bad peer-to-peer exchange arguments");
+      return cudaErrorInvalidValue;
+    }
+    for (int r = 0; r < d.p2p_world; ++r) a.p2p_recv[r] = d.p2p_recv[r];
+    a.p2p_shard = d.p2p_shard;
+    a.p2p_rank = d.p2p_rank;
+    a.p2p_world = d.p2p_world;
+  }
   const bool need_lo = tf && d.epilogue != EPI_F32 && d.epilogue != EPI_TRUNC16;
   if ((d.epilogue == EPI_F32 && !d.out_f32) || (d.epilogue == EPI_TRUNC16 && !d.out) ||
       (d.epilogue == EPI_SGD_APPLY && (!d.out_f32 || !d.out)) ||

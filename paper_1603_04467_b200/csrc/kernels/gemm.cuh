@@ -52,7 +52,11 @@ struct GemmCfg {
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;        // two accumulator buffers
   static constexpr int BAR_BYTES = (2 * STAGES + 8) * 8 + 32;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;  // + alignment slack
+  // EPI_TRUNC16_P2P staging: per epilogue warp a 32-row x 64-column u16 block (row pitch
+  // 72 halves), so peer stores go out as full 128-byte row segments
+  static constexpr int STG_PITCH = 72;
+  static constexpr int STG_BYTES = 4 * 32 * STG_PITCH * 2;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + STG_BYTES + 1024;  // + alignment slack
   static constexpr int SCHED_CONSUMERS = (CG == 2) ? 11 : 6;  // producer x CG + MMA + 4 epilogue warps x CG
   // k-blocks per TMEM accumulation chunk: 3xTF32 flushes every 128 of K into fp32
   // registers (reading A25); bf16 accumulates the whole K in TMEM
@@ -156,6 +160,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* sched_empty = bars + 2 * STAGES + 6;  // [2] tile id consumed (leader; SCHED_CONSUMERS arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
   int* sched_tile = reinterpret_cast<int*>(tmem_slot + 4);  // [2]
+  uint16_t* stg_base = reinterpret_cast<uint16_t*>(bars) + Cfg::BAR_BYTES / 2;  // P2P staging
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -444,6 +449,42 @@ __global__ void __launch_bounds__(256, 1)
                 if (gn + j < args.N) o[j] = static_cast<uint16_t>(r[j] >> 16);
             }
           }
+        } else if constexpr (EPI == EPI_TRUNC16_P2P) {
+          // truncate, stage a 32-row x 64-column block per warp in smem, then push it to the
+          // owners as 128-byte row segments (8 lanes x 16 B per row: full NVLink writes).
+          // 8-element groups never straddle an owner (shard % 8 == 0, N % 8 == 0 on that path)
+          uint16_t* stg = stg_base + q * 32 * Cfg::STG_PITCH;
+          uint32_t* srow = reinterpret_cast<uint32_t*>(stg + lane * Cfg::STG_PITCH + (c & 1) * 32);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) srow[j] = (r[2 * j] >> 16) | (r[2 * j + 1] & 0xFFFF0000u);
+          if (c & 1) {
+            __syncwarp();
+            const int gm0 = tm * (BM * CG) + cta_rank * BM + q * 32;
+            const int gn0 = tn * BN + (c - 1) * 32;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int p = it * 32 + lane, row = p >> 3, seg = p & 7;
+              const int gmr = gm0 + row, gc = gn0 + seg * 8;
+              if (gmr < args.M && gc < args.N) {
+                const int64_t idx = static_cast<int64_t>(gmr) * args.N + gc;
+                const uint16_t* src = stg + row * Cfg::STG_PITCH + seg * 8;
+                if (gc + 8 <= args.N && (args.N % 8) == 0) {
+                  const int owner = static_cast<int>(idx / args.p2p_shard);
+                  uint16_t* dst = args.p2p_recv[owner] + static_cast<int64_t>(args.p2p_rank) * args.p2p_shard +
+                                  (idx - static_cast<int64_t>(owner) * args.p2p_shard);
+                  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+                } else {
+                  for (int e = 0; e < 8 && gc + e < args.N; ++e) {
+                    const int64_t ie = idx + e;
+                    const int owner = static_cast<int>(ie / args.p2p_shard);
+                    args.p2p_recv[owner][static_cast<int64_t>(args.p2p_rank) * args.p2p_shard +
+                                         (ie - static_cast<int64_t>(owner) * args.p2p_shard)] = src[e];
+                  }
+                }
+              }
+            }
+            __syncwarp();
+          }
         } else if constexpr (EPI == EPI_SGD_APPLY) {
           // N = 1: ApplyGradientDescent fused into the dW epilogue (a4 + a9):
           // W <- fl(W - fl(lr * g)) on the fp32 master; the operand copy (bf16 RNE or
@@ -634,6 +675,8 @@ __global__ void __launch_bounds__(256, 1)
       for (int o = 16; o > 0; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
       if (lane == 0 && args.loss_partials) args.loss_partials[blockIdx.x * 4 + q] = loss_acc;
     }
+    // the owners read these NVLink stores after a later kernel's system-scope flag
+    if constexpr (EPI == EPI_TRUNC16_P2P) __threadfence_system();
   }
 
   ptx::tc_fence_before();

@@ -16,7 +16,11 @@ enum GemmEpilogue : int {
   EPI_BIAS_RELU_LOSS = 4,  // a = relu(acc + bias) [-> out_f32]; loss seed dz -> operand out
                            // [+ db partials, + loss partials]                            (a1 + a2 + a5)
   EPI_SGD_APPLY = 5,       // out_f32 (fp32 master W) -= lr * acc; operand copy refreshed  (a4 + a9, N = 1)
+  EPI_TRUNC16_P2P = 6,     // bits(acc) >> 16 stored straight into the OWNER rank's receive slot over
+                           // NVLink (peer pointers): a4 + a6 + the all-to-all leg of a7 in one kernel
 };
+
+constexpr int kMaxRanks = 8;
 
 // Kernel arguments (by value, __grid_constant__-style).
 struct GemmArgs {
@@ -48,6 +52,12 @@ struct GemmArgs {
   double* loss_partials;  // [grid * 4] per-(CTA, epilogue warp) partial sums
   // EPI_RELUGRAD / EPI_BIAS_RELU_LOSS: column sums of the stored dz per 32-row block
   float* colsum_ws;       // [ceil(M / 32), N] or nullptr
+  // EPI_TRUNC16_P2P: element (m, n) is bucket index m*N + n, owned by rank idx / p2p_shard;
+  // it lands at p2p_recv[owner][p2p_rank * p2p_shard + idx - owner * p2p_shard]
+  uint16_t* p2p_recv[kMaxRanks];
+  int64_t p2p_shard;
+  int p2p_rank;
+  int p2p_world;
 };
 
 struct GemmDesc {
@@ -65,6 +75,9 @@ struct GemmDesc {
   double* loss_partials;
   float* colsum_ws;                         // fused db partials (RELUGRAD, BIAS_RELU_LOSS)
   float sgd_lr;                             // EPI_SGD_APPLY
+  uint16_t* const* p2p_recv;                // EPI_TRUNC16_P2P: [world] peer receive bases
+  int64_t p2p_shard;
+  int p2p_rank, p2p_world;
   int group;       // tile-raster group (M tiles); 0 = default
   int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)

@@ -274,7 +274,7 @@ dflow_status alloc_state(dflow_session* s) {
     ly.shard = ly.Ppad / N;
     ST(dmalloc(s, &ly.g32, ly.Ppad));
     ST(dmalloc(s, &ly.colsum_ws, ((cap + 31) / 32) * ly.out));
-    if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+    if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 && !s->p2p) {
       ST(dmalloc(s, &ly.q16, ly.Ppad));
       uint16_t *r, *o, *gt;
       ST(dmalloc(s, &r, ly.Ppad));
@@ -298,7 +298,11 @@ dflow_status alloc_state(dflow_session* s) {
   ST(dmalloc(s, &s->mask_dev, s->mask_words_cap));
   if (cudaMallocHost(&s->loss_host, 4 * sizeof(float)) != cudaSuccess)
     return fail(DFLOW_OOM, "cudaMallocHost failed");
-  if (cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking) != cudaSuccess)
+  // the comm stream gets the highest priority: its exchange kernels take SMs at the next
+  // GEMM boundary instead of queueing behind the following persistent GEMM's CTAs
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if (cudaStreamCreateWithPriority(&s->comm, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
     return fail(DFLOW_CUDA, "stream creation failed");
   s->ev_grad.resize(s->L);
   s->ev_apply.resize(s->L);
@@ -307,6 +311,63 @@ dflow_status alloc_state(dflow_session* s) {
     cudaEventCreateWithFlags(&s->ev_apply[l], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&s->ev_loss, cudaEventDisableTiming);
+  return DFLOW_OK;
+}
+
+// Fused NVLink exchange setup: one symmetric allocation per rank (identical layout on
+// every rank: per layer the receive area [N * shard], the gathered bucket [N * shard]
+// and the flags [2][kMaxRanks]); CUDA IPC handles are exchanged over NCCL and the
+// peers' allocations mapped, so kernels can store into them directly over NVLink.
+dflow_status setup_p2p(dflow_session* s) {
+  const int N = s->opt.world, R = s->opt.rank;
+  if (N > kMaxRanks) return fail(DFLOW_INVALID_ARGUMENT, "the p2p exchange supports up to %d ranks", kMaxRanks);
+  std::vector<size_t> off_recv(s->L), off_gath(s->L), off_flags(s->L);
+  size_t total = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = total;
+    total += (bytes + 255) / 256 * 256;
+    return o;
+  };
+  for (int l = 0; l < s->L; ++l) {
+    off_recv[l] = take(s->layers[l].Ppad * 2);
+    off_gath[l] = take(s->layers[l].Ppad * 2);
+    off_flags[l] = take(2 * kMaxRanks * sizeof(uint32_t));
+  }
+  CU(cudaMalloc(&s->sym, total));
+  CU(cudaMemset(s->sym, 0, total));
+  CU(cudaMalloc(&s->p2p_done, 2 * s->L * sizeof(int)));
+  CU(cudaMemset(s->p2p_done, 0, 2 * s->L * sizeof(int)));
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, s->sym));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  uint8_t* dev = nullptr;
+  CU(cudaMalloc(&dev, 64 * (N + 1)));
+  CU(cudaMemcpy(dev, &h, 64, cudaMemcpyHostToDevice));
+  NC(ncclAllGather(dev, dev + 64, 64, ncclUint8, s->nccl, s->comm));
+  CU(cudaStreamSynchronize(s->comm));
+  std::vector<cudaIpcMemHandle_t> all(N);
+  CU(cudaMemcpy(all.data(), dev + 64, 64 * N, cudaMemcpyDeviceToHost));
+  cudaFree(dev);
+  for (int j = 0; j < N; ++j) {
+    if (j == R) {
+      s->peer_sym[j] = s->sym;
+    } else {
+      CU(cudaIpcOpenMemHandle(&s->peer_sym[j], all[j], cudaIpcMemLazyEnablePeerAccess));
+    }
+  }
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    for (int j = 0; j < N; ++j) {
+      char* b = static_cast<char*>(s->peer_sym[j]);
+      ly.p2p.recv[j] = reinterpret_cast<uint16_t*>(b + off_recv[l]);
+      ly.p2p.gath[j] = reinterpret_cast<uint16_t*>(b + off_gath[l]);
+      ly.p2p.flags[j] = reinterpret_cast<uint32_t*>(b + off_flags[l]);
+    }
+    ly.p2p.done = s->p2p_done + 2 * l;
+    ly.p2p.shard = ly.shard;
+    ly.p2p.rank = R;
+    ly.p2p.world = N;
+  }
   return DFLOW_OK;
 }
 
@@ -391,12 +452,24 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       ST(gemm_plan(s, wa, &ly.wgrad_apply));
       ly.has_wgrad_apply = true;
     }
-    if (s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+    if (s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 && !s->p2p) {
       w.epilogue = EPI_TRUNC16;
       w.out_f32 = nullptr;
       w.out = ly.q16; w.out2 = nullptr; w.ldo = ly.out;
       ST(gemm_plan(s, w, &ly.wgrad16));
       ly.has_wgrad16 = true;
+    }
+    if (s->p2p) {
+      // dW tiles truncated and stored straight into the owners' receive slots (f1)
+      w.epilogue = EPI_TRUNC16_P2P;
+      w.out_f32 = nullptr;
+      w.out = nullptr; w.out2 = nullptr;
+      w.p2p_recv = ly.p2p.recv;
+      w.p2p_shard = ly.p2p.shard;
+      w.p2p_rank = s->opt.rank;
+      w.p2p_world = s->opt.world;
+      ST(gemm_plan(s, w, &ly.wgrad_p2p));
+      ly.has_wgrad_p2p = true;
     }
   }
   s->planned_rows = rows;
@@ -536,6 +609,16 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
     const int t = tbegin(s, 2, cs);
     switch (s->opt.exchange) {
       case DFLOW_EXCHANGE_TRUNC16: {
+        if (s->p2p) {
+          // fused NVLink path: contributions already sit in our receive slots (pushed by the
+          // peers' dW epilogues); fold, push q_bar to every rank, wait for every owner
+          ST(check_launch(s, launch_owner_reduce_p2p(ly.p2p, s->epoch, cs), 1, "owner reduce (p2p)"));
+          ST(check_launch(s, launch_wait_flags(ly.p2p.flags[s->opt.rank] + kMaxRanks, N, s->epoch, cs), 1,
+                          "gather wait (p2p)"));
+          g16 = ly.p2p.gath[s->opt.rank];
+          g32 = nullptr;
+          break;
+        }
         NC(ncclAlltoAll(ly.q16, ly.recv, ly.shard * 2, ncclUint8, s->nccl, cs));
         ST(check_launch(s, launch_owner_reduce_t16(static_cast<uint16_t*>(ly.recv), ly.shard, N,
                                                    static_cast<uint16_t*>(ly.own), cs), 1, "owner reduce"));
@@ -585,12 +668,16 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
   for (int l = s->L - 1; l >= 0; --l) {
     Layer& ly = s->layers[l];
     if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
-    ST(launch_gemm(s, t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32), st));
+    const bool p2p = t16 && s->p2p;
+    ST(launch_gemm(s, p2p ? ly.wgrad_p2p
+                          : t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32),
+                   st));
     // db_l: the producing epilogue left per-32-row column partials; sum them in order
     const int t = tbegin(s, 1, st);
-    cudaError_t e = launch_colsum_final(ly.colsum_ws, static_cast<int>((rows + 31) / 32), ly.out,
-                                        t16 ? nullptr : ly.g32 + ly.in * ly.out,
-                                        t16 ? ly.q16 + ly.in * ly.out : nullptr, st);
+    const int chunks = static_cast<int>((rows + 31) / 32);
+    cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, st)
+                        : launch_colsum_final(ly.colsum_ws, chunks, ly.out, t16 ? nullptr : ly.g32 + ly.in * ly.out,
+                                              t16 ? ly.q16 + ly.in * ly.out : nullptr, st);
     tend(s, t, st);
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
     if (mode == 0) ST(exchange_apply(s, l, st));
@@ -661,6 +748,7 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   s->cap = opt.max_local_rows;
   s->tf32 = opt.precision == DFLOW_PRECISION_3XTF32;
   s->esz = s->tf32 ? 4 : 2;
+  s->p2p = opt.p2p && opt.world > 1 && opt.exchange == DFLOW_EXCHANGE_TRUNC16;
   dflow_status st = insert_exchange(user, opt.world, opt.exchange, &s->g, &s->remap);
   if (st == DFLOW_OK) st = match_graph(s);
   if (st == DFLOW_OK && s->tf32 && s->x_dtype != DFLOW_F32)
@@ -693,6 +781,7 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     ncclResult_t r = ncclCommInitRank(&s->nccl, opt.world, id, opt.rank);
     if (r != ncclSuccess) st = fail(DFLOW_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
   }
+  if (st == DFLOW_OK && s->p2p) st = setup_p2p(s);
   if (st != DFLOW_OK) {
     session_destroy(s);
     return st;
@@ -705,6 +794,10 @@ void session_destroy(dflow_session* s) {
   if (!s) return;
   cudaSetDevice(s->opt.device);
   cudaDeviceSynchronize();
+  for (int j = 0; j < dflow::kMaxRanks; ++j)
+    if (s->peer_sym[j] && s->peer_sym[j] != s->sym) cudaIpcCloseMemHandle(s->peer_sym[j]);
+  if (s->sym) cudaFree(s->sym);
+  if (s->p2p_done) cudaFree(s->p2p_done);
   if (s->nccl) ncclCommDestroy(s->nccl);
   for (Layer& ly : s->layers) {
     for (void* p : {(void*)ly.W32, (void*)ly.b32, (void*)ly.g32, (void*)ly.q16, ly.recv, ly.own, ly.gath,
@@ -715,7 +808,8 @@ void session_destroy(dflow_session* s) {
     free_operand(ly.dZ);
   }
   free_operand(s->A0);
-  for (void* p : {(void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0], s->host_stage[1]})
+  for (void* p : {(void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0],
+                  s->host_stage[1], s->xbuf[0], s->xbuf[1], s->xbuf[2], s->xbuf[3]})
     if (p) cudaFree(p);
   if (s->loss_host) cudaFreeHost(s->loss_host);
   for (cudaEvent_t e : s->ev_grad) cudaEventDestroy(e);
@@ -734,6 +828,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   Feeds f;
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
   s->launches = s->gemm_launches = 0;
+  s->epoch++;  // p2p exchange flags of this step
   ST(run_forward(s, f, rows, st, FWD_TRAIN));
   ST(run_backward(s, rows, st, 0));
   CU(cudaGetLastError());
@@ -924,12 +1019,19 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
     return DFLOW_OK;
   }
   const int64_t npad = pad_to(static_cast<int64_t>(n), 8 * N), shard = npad / N;
-  void *send = nullptr, *recv = nullptr, *own = nullptr, *gath = nullptr;
   const size_t esz = s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 ? 2 : 4;
-  CU(cudaMalloc(&send, npad * esz));
-  CU(cudaMalloc(&recv, npad * esz));
-  CU(cudaMalloc(&own, shard * esz));
-  CU(cudaMalloc(&gath, npad * esz));
+  if (s->xbuf_bytes < static_cast<size_t>(npad) * 4) {  // grow-only scratch (send, recv, own, gath)
+    CU(cudaStreamSynchronize(st));
+    CU(cudaStreamSynchronize(s->comm));
+    for (void*& p : s->xbuf) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    s->xbuf_bytes = 0;
+    for (void*& p : s->xbuf) CU(cudaMalloc(&p, static_cast<size_t>(npad) * 4));
+    s->xbuf_bytes = static_cast<size_t>(npad) * 4;
+  }
+  void *send = s->xbuf[0], *recv = s->xbuf[1], *own = s->xbuf[2], *gath = s->xbuf[3];
   CU(cudaMemsetAsync(send, 0, npad * esz, st));
   cudaError_t e = cudaSuccess;
   if (s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
@@ -956,11 +1058,9 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
     CU(launch_scale_f32(static_cast<float*>(gath), npad, 1.0f / N, cs));
     CU(cudaMemcpyAsync(out, gath, n * sizeof(float), cudaMemcpyDeviceToDevice, cs));
   }
-  CU(cudaStreamSynchronize(cs));
-  cudaFree(send);
-  cudaFree(recv);
-  cudaFree(own);
-  cudaFree(gath);
+  // stream-ordered completion: later work on `st` sees `out`
+  CU(cudaEventRecord(s->ev_loss, cs));
+  CU(cudaStreamWaitEvent(st, s->ev_loss, 0));
   return DFLOW_OK;
 }
 

@@ -10,6 +10,7 @@
 
 #include "../../include/dflow.h"
 #include "graph.h"
+#include "kernels/exchange_p2p.h"
 #include "kernels/gemm.h"
 
 namespace dflow {
@@ -47,8 +48,9 @@ struct Layer {
   void* own = nullptr;            // owner's reduced shard [shard]
   void* gath = nullptr;           // allgather landing [Ppad]
   float* colsum_ws = nullptr;     // fused db partials [ceil(cap/32), out]
-  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16, wgrad_apply;
-  bool has_fwd = false, has_dgrad = false, has_wgrad16 = false, has_wgrad_apply = false;
+  P2PLayer p2p;                   // fused NVLink exchange: peer pointers of this layer
+  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16, wgrad_apply, wgrad_p2p;
+  bool has_fwd = false, has_dgrad = false, has_wgrad16 = false, has_wgrad_apply = false, has_wgrad_p2p = false;
 };
 
 struct TimedRange {
@@ -81,12 +83,20 @@ struct dflow_session {
   float* loss_host = nullptr;     // pinned
   uint32_t* mask_dev = nullptr;
   int64_t mask_words_cap = 0;
+  void* xbuf[4] = {nullptr, nullptr, nullptr, nullptr};  // dflow_exchange scratch (grow-only)
+  size_t xbuf_bytes = 0;
   void* host_stage[2] = {nullptr, nullptr};  // device copies of host feeds (e2e path)
   size_t host_stage_bytes[2] = {0, 0};
   cudaStream_t comm = nullptr;
   std::vector<cudaEvent_t> ev_grad, ev_apply;
   cudaEvent_t ev_loss = nullptr;
   ncclComm_t nccl = nullptr;
+  // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
+  bool p2p = false;
+  void* sym = nullptr;
+  void* peer_sym[dflow::kMaxRanks] = {};
+  int* p2p_done = nullptr;
+  uint32_t epoch = 0;
   bool poisoned = false;
   bool have_forward = false;
   int64_t last_rows = 0;

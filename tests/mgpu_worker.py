@@ -30,6 +30,9 @@ import synth  # noqa: E402
 
 
 def main(out_path, exchange):
+    p2p = 0
+    if exchange == "TRUNC16_P2P":  # the fused NVLink exchange (f1): same bits as the NCCL path
+        exchange, p2p = "TRUNC16", 1
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -39,14 +42,15 @@ def main(out_path, exchange):
         idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(idt, 0)
     nid = bytes(idt.cpu().numpy().tobytes())
-    verdict = {"world": world, "exchange": exchange}
+    verdict = {"world": world, "exchange": exchange, "p2p": p2p}
 
     w = synth.with_batch(synth.C2, 256)
     b = w.batch // world
     Ws, bs = synth.init_params(w)
     X, Y = synth.batch(w)
     Xr, Yr = X[rank * b:(rank + 1) * b], Y[rank * b:(rank + 1) * b]
-    run = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local, nccl_id=nid)
+    run = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local, nccl_id=nid,
+              p2p=p2p)
     run.assign(Ws, bs)
     Xd, Yd = torch.from_numpy(Xr).cuda(), torch.from_numpy(Yr).cuda()
 

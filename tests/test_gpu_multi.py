@@ -31,7 +31,7 @@ def _run(n, exchange, tmp_path):
     return json.load(open(out))
 
 
-@pytest.mark.parametrize("exchange", ["TRUNC16", "FP32", "FP32_NCCL"])
+@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL"])
 def test_two_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 2:
@@ -45,11 +45,12 @@ def test_two_gpu_replicated_step(exchange, tmp_path):
     assert v["w_after_max_err"] < 2e-2, v
 
 
-def test_four_gpu_replicated_step(tmp_path):
+@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P"])
+def test_four_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
-    v = _run(4, "TRUNC16", tmp_path)
+    v = _run(4, exchange, tmp_path)
     print(v)
     assert v["p4_exchange_ok"] and v["p4_step_bitexact"] and v["p11_after_4_steps"], v
     assert v["w_after_max_err"] < 2e-2, v
