@@ -51,7 +51,10 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;        // two accumulator buffers
-  static constexpr int BAR_BYTES = (2 * STAGES + 8) * 8 + 32;
+  // tile-id ring depth: the producer runs ~1 tile ahead of the MMA and the epilogue ~1 tile
+  // behind it, so the ring must hold >= 3 ids or the producer stalls at tile boundaries
+  static constexpr int SCHED_DEPTH = 4;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_DEPTH) * 8 + 16 + 4 * SCHED_DEPTH;
   // EPI_TRUNC16_P2P staging: per epilogue warp a 32-row x 64-column u16 block (row pitch
   // 72 halves), so peer stores go out as full 128-byte row segments
   static constexpr int STG_PITCH = 72;
@@ -156,10 +159,11 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* empty = bars + STAGES;
   uint64_t* tfull = bars + 2 * STAGES;
   uint64_t* tempty = bars + 2 * STAGES + 2;
-  uint64_t* sched_full = bars + 2 * STAGES + 4;   // [2] tile id published (count 1)
-  uint64_t* sched_empty = bars + 2 * STAGES + 6;  // [2] tile id consumed (leader; SCHED_CONSUMERS arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 8);
-  int* sched_tile = reinterpret_cast<int*>(tmem_slot + 4);  // [2]
+  constexpr int SD = Cfg::SCHED_DEPTH;
+  uint64_t* sched_full = bars + 2 * STAGES + 4;        // [SD] tile id published (count 1)
+  uint64_t* sched_empty = bars + 2 * STAGES + 4 + SD;  // [SD] tile id consumed (leader; SCHED_CONSUMERS arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4 + 2 * SD);
+  int* sched_tile = reinterpret_cast<int*>(tmem_slot + 4);  // [SD]
   uint16_t* stg_base = reinterpret_cast<uint16_t*>(bars) + Cfg::BAR_BYTES / 2;  // P2P staging
 
   const int warp = threadIdx.x >> 5;
@@ -184,8 +188,10 @@ __global__ void __launch_bounds__(256, 1)
       if constexpr (CG == 2) ptx::mbar_arrive_cluster(sched_empty_leader + slot * 8);
       else ptx::mbar_arrive(ptx::smem_u32(&sched_empty[slot]));
     }
-    slot ^= 1;
-    if (slot == 0) ph ^= 1;
+    if (++slot == SD) {
+      slot = 0;
+      ph ^= 1;
+    }
     return t;
   };
 
@@ -205,6 +211,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(ptx::smem_u32(&tfull[a]), 1);
       ptx::mbar_init(ptx::smem_u32(&tempty[a]), 4 * CG);
+    }
+    for (int a = 0; a < SD; ++a) {
       ptx::mbar_init(ptx::smem_u32(&sched_full[a]), 1);
       ptx::mbar_init(ptx::smem_u32(&sched_empty[a]), Cfg::SCHED_CONSUMERS);
     }
@@ -350,8 +358,10 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (t >= num_tiles) break;
         t = args.sched ? num_clusters + atomicAdd(&args.sched[0], 1) : t + num_clusters;
-        slot ^= 1;
-        if (slot == 0) ph ^= 1;
+        if (++slot == SD) {
+          slot = 0;
+          ph ^= 1;
+        }
       }
       if (args.sched) {
         // the last cluster to finish resets the counters for the next launch on this stream
