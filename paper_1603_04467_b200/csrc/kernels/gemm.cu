@@ -61,31 +61,33 @@ static bool make_tmap(CUtensorMap* m, const void* base, bool f32, int64_t inner,
 }
 
 template <int BN, int CG, bool TF32, bool A_MN, bool B_MN, int EPI>
-static void* kernel_ptr() {
+static void* kernel_ptr(int* smem) {
   auto k = &gemm_kernel<BN, CG, TF32, A_MN, B_MN, EPI>;
+  constexpr int bytes = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P>::SMEM_BYTES;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN, CG, TF32>::SMEM_BYTES);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     attr_set = true;
   }
+  *smem = bytes;
   return reinterpret_cast<void*>(k);
 }
 
 // The (operand majors, epilogue) combinations the MLP step uses, per tile config.
 template <int BN, int CG, bool TF32>
-static void* select_kernel(bool a_mn, bool b_mn, int epi) {
+static void* select_kernel(bool a_mn, bool b_mn, int epi, int* smem) {
   if (!a_mn && b_mn) {  // forward: A K-major, W MN-major
-    if (epi == EPI_BIAS_RELU) return kernel_ptr<BN, CG, TF32, false, true, EPI_BIAS_RELU>();
-    if (epi == EPI_BIAS_RELU_LOSS) return kernel_ptr<BN, CG, TF32, false, true, EPI_BIAS_RELU_LOSS>();
-    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, true, EPI_F32>();
+    if (epi == EPI_BIAS_RELU) return kernel_ptr<BN, CG, TF32, false, true, EPI_BIAS_RELU>(smem);
+    if (epi == EPI_BIAS_RELU_LOSS) return kernel_ptr<BN, CG, TF32, false, true, EPI_BIAS_RELU_LOSS>(smem);
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, true, EPI_F32>(smem);
   } else if (!a_mn && !b_mn) {  // dgrad: dZ K-major, W K-major
-    if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, TF32, false, false, EPI_RELUGRAD>();
-    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, false, EPI_F32>();
+    if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, TF32, false, false, EPI_RELUGRAD>(smem);
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, false, EPI_F32>(smem);
   } else if (a_mn && b_mn) {  // wgrad: activations and dZ both MN-major
-    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, true, true, EPI_F32>();
-    if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16>();
-    if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, TF32, true, true, EPI_SGD_APPLY>();
-    if (epi == EPI_TRUNC16_P2P) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16_P2P>();
+    if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, true, true, EPI_F32>(smem);
+    if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16>(smem);
+    if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, TF32, true, true, EPI_SGD_APPLY>(smem);
+    if (epi == EPI_TRUNC16_P2P) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16_P2P>(smem);
   }
   return nullptr;
 }
@@ -136,17 +138,17 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   plan->tiles_n = static_cast<int>((d.N + BN - 1) / BN);
   void* k = nullptr;
   if (tile == 2)
-    k = tf ? select_kernel<128, 2, true>(d.a_mn, d.b_mn, d.epilogue) : select_kernel<256, 2, false>(d.a_mn, d.b_mn, d.epilogue);
+    k = tf ? select_kernel<128, 2, true>(d.a_mn, d.b_mn, d.epilogue, &plan->smem)
+           : select_kernel<256, 2, false>(d.a_mn, d.b_mn, d.epilogue, &plan->smem);
   else
-    k = tf ? select_kernel<128, 1, true>(d.a_mn, d.b_mn, d.epilogue) : select_kernel<128, 1, false>(d.a_mn, d.b_mn, d.epilogue);
+    k = tf ? select_kernel<128, 1, true>(d.a_mn, d.b_mn, d.epilogue, &plan->smem)
+           : select_kernel<128, 1, false>(d.a_mn, d.b_mn, d.epilogue, &plan->smem);
   if (!k) {
     snprintf(g_err, sizeof g_err, "unsupported GEMM layout/epilogue (a_mn=%d b_mn=%d epi=%d)", d.a_mn, d.b_mn,
              d.epilogue);
     return cudaErrorInvalidValue;
   }
   plan->kernel = k;
-  plan->smem = (tile == 2) ? (tf ? GemmCfg<128, 2, true>::SMEM_BYTES : GemmCfg<256, 2, false>::SMEM_BYTES)
-                           : (tf ? GemmCfg<128, 1, true>::SMEM_BYTES : GemmCfg<128, 1, false>::SMEM_BYTES);
   const int64_t K = d.K > 0 ? d.K : 1;
   // MN-major fp32 (tf32) operands: 32-byte-atom 128B swizzle (the UMMA SWIZZLE_128B_BASE32B layout)
   auto map_a = [&](CUtensorMap* m, const void* p) {
@@ -194,6 +196,11 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.vec_y = aligned16(d.y, d.ldy, 4) ? 1 : 0;
   a.group_m = d.group > 0 ? d.group : 8;
   if (const char* e = getenv("DFLOW_GEMM_GROUP")) a.group_m = atoi(e) > 0 ? atoi(e) : a.group_m;
+  // L2 prefetch distance in k-blocks (DFLOW_GEMM_PREFETCH). Off by default: measured on the
+  // C3 shapes it costs 20-25% (the extra L2 lookups contend with the loads; profiles/r1_gemm_issue.md)
+  a.prefetch = 0;
+  if (const char* e = getenv("DFLOW_GEMM_PREFETCH")) a.prefetch = atoi(e) >= 0 ? atoi(e) : a.prefetch;
+  if (const char* e = getenv("DFLOW_GEMM_DEBUG")) a.debug = atoi(e);
   a.sgd_lr = d.sgd_lr;
   a.sched = default_sched();
   if (!a.sched) {

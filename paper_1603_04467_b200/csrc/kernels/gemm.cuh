@@ -37,7 +37,7 @@
 
 namespace dflow {
 
-template <int BN, int CG, bool TF32>
+template <int BN, int CG, bool TF32, bool STG = false>
 struct GemmCfg {
   static constexpr int E = TF32 ? 4 : 2;          // operand element bytes
   static constexpr int BM = 128;                  // rows per CTA
@@ -49,18 +49,24 @@ struct GemmCfg {
   static constexpr int A_TILE = BM * BK * E;      // 16 KB
   static constexpr int B_TILE = BN_CTA * BK * E;  // 16 KB (BN_CTA = 128)
   static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);
-  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;        // two accumulator buffers
   // tile-id ring depth: the producer runs ~1 tile ahead of the MMA and the epilogue ~1 tile
   // behind it, so the ring must hold >= 3 ids or the producer stalls at tile boundaries
   static constexpr int SCHED_DEPTH = 4;
-  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_DEPTH) * 8 + 16 + 4 * SCHED_DEPTH;
+  static constexpr int BAR_BYTES_MAX = (2 * 8 + 4 + 2 * SCHED_DEPTH) * 8 + 16 + 4 * SCHED_DEPTH;
   // EPI_TRUNC16_P2P staging: per epilogue warp a 32-row x 64-column u16 block (row pitch
   // 72 halves), so peer stores go out as full 128-byte row segments
   static constexpr int STG_PITCH = 72;
-  static constexpr int STG_BYTES = 4 * 32 * STG_PITCH * 2;
+  static constexpr int STG_BYTES = STG ? 4 * 32 * STG_PITCH * 2 : 0;
+  // as many pipeline stages as the 227 KB opt-in shared memory holds (bf16 256x256 pair: 7,
+  // or 6 beside the P2P staging; 3xTF32: 4)
+  static constexpr int SMEM_MAX = 227 * 1024;
+  static constexpr int STAGE_BUDGET = SMEM_MAX - 1024 - BAR_BYTES_MAX - STG_BYTES;
+  static constexpr int STAGES = STAGE_BUDGET / STAGE_BYTES > 8 ? 8 : STAGE_BUDGET / STAGE_BYTES;
+  static constexpr int BAR_BYTES = (2 * STAGES + 4 + 2 * SCHED_DEPTH) * 8 + 16 + 4 * SCHED_DEPTH;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + STG_BYTES + 1024;  // + alignment slack
-  static constexpr int SCHED_CONSUMERS = (CG == 2) ? 11 : 6;  // producer x CG + MMA + 4 epilogue warps x CG
+  static_assert(SMEM_BYTES <= SMEM_MAX, "shared memory budget");
+  static constexpr int SCHED_CONSUMERS = (CG == 2) ? 11 : 6;  // producer warp x CG + MMA warp + 4 epilogue warps x CG
   // k-blocks per TMEM accumulation chunk: 3xTF32 flushes every 128 of K into fp32
   // registers (reading A25); bf16 accumulates the whole K in TMEM
   static constexpr int KB_PER_CHUNK = TF32 ? 4 : (1 << 30);
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(256, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                 const GemmArgs args) {
-  using Cfg = GemmCfg<BN, CG, TF32>;
+  using Cfg = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, BN_CTA = Cfg::BN_CTA, STAGES = Cfg::STAGES;
   constexpr int A_TILE = Cfg::A_TILE, B_TILE = Cfg::B_TILE, STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr int CHUNK = Cfg::CHUNK, KMMA = Cfg::KMMA, NOPS = Cfg::NOPS;
@@ -225,58 +231,121 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
-    if (lane == 0) {
+    // ===================== TMA producer (warp-uniform; one elected lane issues) =====================
+    {
       int stage = 0;
       uint32_t phase = 0;
       int sslot = 0;
       uint32_t sph = 0;
       const uint32_t full0_local = ptx::smem_u32(&full[0]);
       const uint32_t full0 = (CG == 2) ? ptx::mapa_shared(full0_local, 0) : full0_local;
-      for (;;) {
-        const int t = next_tile(sslot, sph, false);
-        if (t >= num_tiles) break;
+      const uint32_t s_tiles = ptx::smem_u32(tiles);
+      // This CTA's (m0, n0) of tile t.
+      auto origin = [&](int t, int& m0, int& n0) {
         int tm, tn;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
-        const int m0 = tm * (BM * CG) + cta_rank * BM;
-        const int n0 = tn * BN + cta_rank * BN_CTA;
-        for (int kb = 0; kb < num_kb; ++kb) {
-          ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1);
-          const uint32_t fb = full0 + stage * 8;
-          if (cta_rank == 0) ptx::mbar_arrive_expect_tx(ptx::smem_u32(&full[stage]), CG * STAGE_BYTES);
-          const uint32_t s0 = ptx::smem_u32(tiles + stage * STAGE_BYTES);
-          const int k0 = kb * BK;
+        m0 = tm * (BM * CG) + cta_rank * BM;
+        n0 = tn * BN + cta_rank * BN_CTA;
+      };
+      // L2 prefetch cursor: walks the same (tile, k-block) sequence `pf` k-blocks ahead of
+      // the loads, so the loads hit L2 instead of waiting out DRAM latency. It draws the tile
+      // ids from the scheduler ring (one tile ahead of the loads, which take them from t_next).
+      const int pf = (args.prefetch > 0 && num_kb > args.prefetch) ? args.prefetch : 0;
+      int t = next_tile(sslot, sph, true);
+      int pt = t, pkb = 0, pm0 = 0, pn0 = 0, t_next = t;
+      if (pf && pt < num_tiles) origin(pt, pm0, pn0);
+      auto prefetch_step = [&]() {
+        if (pt >= num_tiles) return;
+        const int k0 = pkb * BK;
+        if (ptx::elect_one()) {
 #pragma unroll
           for (int part = 0; part < NOPS; ++part) {
             const CUtensorMap* ma = part ? &tmA2 : &tmA;
             const CUtensorMap* mb = part ? &tmB2 : &tmB;
-            const uint32_t sa = s0 + part * A_TILE;
-            const uint32_t sb = s0 + NOPS * A_TILE + part * B_TILE;
 #pragma unroll
-            for (int i = 0; i < (A_MN ? BM / CHUNK : 1); ++i) {
-              const uint32_t dst = sa + i * CHUNK_BYTES;
-              const int c0 = A_MN ? (m0 + CHUNK * i) : k0;
-              const int c1 = A_MN ? k0 : m0;
-              if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, ma, fb, c0, c1);
-              else ptx::tma_load_2d(dst, ma, fb, c0, c1);
-            }
+            for (int i = 0; i < (A_MN ? BM / CHUNK : 1); ++i)
+              ptx::tma_prefetch_2d(ma, A_MN ? (pm0 + CHUNK * i) : k0, A_MN ? k0 : pm0);
 #pragma unroll
-            for (int i = 0; i < (B_MN ? BN_CTA / CHUNK : 1); ++i) {
-              const uint32_t dst = sb + i * CHUNK_BYTES;
-              const int c0 = B_MN ? (n0 + CHUNK * i) : k0;
-              const int c1 = B_MN ? k0 : n0;
-              if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, mb, fb, c0, c1);
-              else ptx::tma_load_2d(dst, mb, fb, c0, c1);
+            for (int i = 0; i < (B_MN ? BN_CTA / CHUNK : 1); ++i)
+              ptx::tma_prefetch_2d(mb, B_MN ? (pn0 + CHUNK * i) : k0, B_MN ? k0 : pn0);
+          }
+        }
+        __syncwarp();
+        if (++pkb == num_kb) {
+          pkb = 0;
+          pt = next_tile(sslot, sph, true);
+          t_next = pt;
+          if (pt < num_tiles) origin(pt, pm0, pn0);
+        }
+      };
+      for (int i = 0; i < pf; ++i) prefetch_step();
+      while (t < num_tiles) {
+        int m0, n0;
+        origin(t, m0, n0);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          if (pf) prefetch_step();
+          if (args.debug & 4) ptx::mbar_wait_spin(ptx::smem_u32(&empty[stage]), phase ^ 1);
+          else ptx::mbar_wait(ptx::smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = full0 + stage * 8;
+          const uint32_t s0 = s_tiles + stage * STAGE_BYTES;
+          const int k0 = kb * BK;
+          if (ptx::elect_one()) {
+            if (args.debug & 1) {  // profiling: MMA on stale smem, no TMA traffic
+              if (cta_rank == 0) ptx::mbar_arrive(ptx::smem_u32(&full[stage]));
+            } else {
+              if (cta_rank == 0) ptx::mbar_arrive_expect_tx(ptx::smem_u32(&full[stage]), CG * STAGE_BYTES);
+#pragma unroll
+              for (int part = 0; part < NOPS; ++part) {
+                const CUtensorMap* ma = part ? &tmA2 : &tmA;
+                const CUtensorMap* mb = part ? &tmB2 : &tmB;
+                const uint32_t sa = s0 + part * A_TILE;
+                const uint32_t sb = s0 + NOPS * A_TILE + part * B_TILE;
+#pragma unroll
+                for (int i = 0; i < (A_MN ? BM / CHUNK : 1); ++i) {
+                  const uint32_t dst = sa + i * CHUNK_BYTES;
+                  const int c0 = A_MN ? (m0 + CHUNK * i) : k0;
+                  const int c1 = A_MN ? k0 : m0;
+                  if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, ma, fb, c0, c1);
+                  else ptx::tma_load_2d(dst, ma, fb, c0, c1);
+                }
+#pragma unroll
+                for (int i = 0; i < (B_MN ? BN_CTA / CHUNK : 1); ++i) {
+                  const uint32_t dst = sb + i * CHUNK_BYTES;
+                  const int c0 = B_MN ? (n0 + CHUNK * i) : k0;
+                  const int c1 = B_MN ? k0 : n0;
+                  if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, mb, fb, c0, c1);
+                  else ptx::tma_load_2d(dst, mb, fb, c0, c1);
+                }
+              }
             }
           }
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        t = pf ? t_next : next_tile(sslot, sph, true);
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer (one thread of the leader CTA) =====================
-    if (cta_rank == 0 && lane == 0) {
+    // ===================== MMA issuer (leader CTA; warp-uniform, one elected lane issues) =====================
+    if (cta_rank == 0) {
       constexpr uint32_t idesc = ptx::make_idesc(BM * CG, BN, A_MN, B_MN, TF32);
+      // smem descriptors of stage 0; a stage / k step only moves the start address
+      // (field [0,14) = addr >> 4, < 2^14 for any shared address, so plain adds never carry)
+      auto mn_desc = [&](uint32_t addr) {
+        // MN-major tf32 operands use the 32-byte-atom 128B swizzle (4-row period, SBO = 4 rows)
+        return TF32 ? ptx::smem_desc_sw128_base32(addr, CHUNK_BYTES, 512) : ptx::smem_desc_sw128(addr, CHUNK_BYTES, 1024);
+      };
+      const uint32_t s_tiles = ptx::smem_u32(tiles);
+      uint64_t a_desc0[NOPS], b_desc0[NOPS];
+#pragma unroll
+      for (int part = 0; part < NOPS; ++part) {
+        const uint32_t a = s_tiles + part * A_TILE;
+        const uint32_t b = s_tiles + NOPS * A_TILE + part * B_TILE;
+        a_desc0[part] = A_MN ? mn_desc(a) : ptx::smem_desc_sw128(a, 16, 1024);
+        b_desc0[part] = B_MN ? mn_desc(b) : ptx::smem_desc_sw128(b, 16, 1024);
+      }
+      constexpr uint32_t KA_STEP = (A_MN ? KMMA * 128 : 32) >> 4;
+      constexpr uint32_t KB_STEP = (B_MN ? KMMA * 128 : 32) >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -284,7 +353,7 @@ __global__ void __launch_bounds__(256, 1)
       int sslot = 0;
       uint32_t sph = 0;
       for (;;) {
-        const int t = next_tile(sslot, sph, false);
+        const int t = next_tile(sslot, sph, true);
         if (t >= num_tiles) break;
         if (num_kb == 0) continue;
         // K is processed in chunks, each accumulated from zero into one of the two TMEM
@@ -299,40 +368,30 @@ __global__ void __launch_bounds__(256, 1)
             ptx::tc_fence_after();
             d = tmem_base + acc * BN;
           }
-          ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
+          if (args.debug & 4) ptx::mbar_wait_spin(ptx::smem_u32(&full[stage]), phase);
+          else ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
           ptx::tc_fence_after();
-          const uint32_t s0 = ptx::smem_u32(tiles + stage * STAGE_BYTES);
+          const uint64_t soff = static_cast<uint64_t>((stage * STAGE_BYTES) >> 4);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / KMMA; ++k) {
-            const uint32_t ka = A_MN ? k * KMMA * 128 : k * 32;
-            const uint32_t kbo = B_MN ? k * KMMA * 128 : k * 32;
-            // MN-major tf32 operands use the 32-byte-atom 128B swizzle (4-row period, SBO = 4 rows)
-            auto mn_desc = [&](uint32_t addr) {
-              return TF32 ? ptx::smem_desc_sw128_base32(addr, CHUNK_BYTES, 512)
-                          : ptx::smem_desc_sw128(addr, CHUNK_BYTES, 1024);
-            };
-            auto adesc = [&](int part) {
-              const uint32_t a = s0 + part * A_TILE + ka;
-              return A_MN ? mn_desc(a) : ptx::smem_desc_sw128(a, 16, 1024);
-            };
-            auto bdesc = [&](int part) {
-              const uint32_t b = s0 + NOPS * A_TILE + part * B_TILE + kbo;
-              return B_MN ? mn_desc(b) : ptx::smem_desc_sw128(b, 16, 1024);
-            };
-            const uint32_t first = (chunk_start && k == 0) ? 0u : 1u;
-            if constexpr (TF32) {
-              // small products first (reading A14), then big * big
-              ptx::mma_ss<CG, true>(d, adesc(0), bdesc(1), idesc, first);
-              ptx::mma_ss<CG, true>(d, adesc(1), bdesc(0), idesc, 1u);
-              ptx::mma_ss<CG, true>(d, adesc(0), bdesc(0), idesc, 1u);
-            } else {
-              ptx::mma_ss<CG, false>(d, adesc(0), bdesc(0), idesc, first);
+            for (int k = 0; k < BK / KMMA; ++k) {
+              const uint32_t first = (chunk_start && k == 0) ? 0u : 1u;
+              const uint64_t ao = soff + k * KA_STEP, bo = soff + k * KB_STEP;
+              if constexpr (TF32) {
+                // small products first (reading A14), then big * big
+                ptx::mma_ss<CG, true>(d, a_desc0[0] + ao, b_desc0[1] + bo, idesc, first);
+                ptx::mma_ss<CG, true>(d, a_desc0[1] + ao, b_desc0[0] + bo, idesc, 1u);
+                ptx::mma_ss<CG, true>(d, a_desc0[0] + ao, b_desc0[0] + bo, idesc, 1u);
+              } else {
+                ptx::mma_ss<CG, false>(d, a_desc0[0] + ao, b_desc0[0] + bo, idesc, first);
+              }
             }
+            ptx::mma_commit<CG>(ptx::smem_u32(&empty[stage]), 0x3);
+            if (chunk_end) ptx::mma_commit<CG>(ptx::smem_u32(&tfull[acc]), 0x3);
           }
-          ptx::mma_commit<CG>(ptx::smem_u32(&empty[stage]), 0x3);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (chunk_end) {
-            ptx::mma_commit<CG>(ptx::smem_u32(&tfull[acc]), 0x3);
             acc ^= 1;
             if (acc == 0) acc_phase ^= 1;
           }
@@ -422,6 +481,10 @@ __global__ void __launch_bounds__(256, 1)
       } else if (num_kb > 0) {
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
         ptx::tc_fence_after();
+        if (args.debug & 2) {  // profiling: hand the accumulator straight back
+          release_tmem();
+          continue;
+        }
       }
       auto column_chunk = [&](int c, uint32_t (&r)[32]) {
         const int gn = tn * BN + c * 32;

@@ -46,6 +46,9 @@ struct GemmArgs {
   int denom_pow2;         // 1: loss_denom is a power of two, so d * inv_denom == d / loss_denom
   int vec_y;              // 1: 16-byte vector loads are aligned for y
   int group_m;            // tile raster: M-tiles per group (L2 reuse of the B panels)
+  int prefetch;           // k-blocks the producer's L2 prefetch runs ahead of its loads (0: off)
+  int debug;              // profiling only (DFLOW_GEMM_DEBUG): 1 no TMA loads, 2 no epilogue work,
+                          // 4 hint-free barrier waits in the producer / MMA loop
   int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
   float seed_const;       // 1 / rows (SUM seed)
   float sgd_lr;           // EPI_SGD_APPLY learning rate

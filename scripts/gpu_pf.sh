@@ -1,0 +1,7 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_step.py tests/test_gpu_tf32.py -q -m gpu -x 2>&1 | tail -3
+timeout 600 python scripts/gemm_sweep.py --groups 8 --prefetch 0,4,8,16 --reps 20 > gpurun_out/pf_sweep.json 2>&1; cat gpurun_out/pf_sweep.json
+timeout 600 python scripts/gemm_sweep.py --groups 8 --prefetch 0,8 --reps 2 --no-cublas > /dev/null 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,sm__cycles_elapsed.avg.per_second,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active,lts__t_sector_hit_rate.pct --clock-control none --csv --log-file gpurun_out/pf_ncu.csv python scripts/gemm_sweep.py --groups 8 --prefetch 0,8 --reps 2 > gpurun_out/pf_ncu.log 2>&1; echo rc=$?
+timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo rc=$?; cat gpurun_out/bench.json; tail -3 gpurun_out/bench.err
