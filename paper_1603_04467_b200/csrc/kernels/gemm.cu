@@ -194,6 +194,7 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.denom_pow2 = (mn > 0 && (mn & (mn - 1)) == 0) ? 1 : 0;
   a.inv_denom = 1.0f / a.loss_denom;
   a.vec_y = aligned16(d.y, d.ldy, 4) ? 1 : 0;
+  a.vec_bias = aligned16(d.bias, 0, 4) ? 1 : 0;
   a.group_m = d.group > 0 ? d.group : 8;
   if (const char* e = getenv("DFLOW_GEMM_GROUP")) a.group_m = atoi(e) > 0 ? atoi(e) : a.group_m;
   // L2 prefetch distance in k-blocks (DFLOW_GEMM_PREFETCH). Off by default: measured on the

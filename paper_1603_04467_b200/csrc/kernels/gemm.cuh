@@ -486,7 +486,24 @@ __global__ void __launch_bounds__(256, 1)
           continue;
         }
       }
-      auto column_chunk = [&](int c, uint32_t (&r)[32]) {
+      // EPI_BIAS_RELU_LOSS: the 32 targets y[gm, gn .. gn+31] of a column chunk, loaded one
+      // chunk ahead of its use so the DRAM latency overlaps the previous chunk's work
+      auto load_y = [&](int c, float (&yv)[32]) {
+        const int gn = tn * BN + c * 32;
+        if (args.loss_kind != 0 || !row_ok || gn >= args.N) return;
+        const float* yrow = args.y + static_cast<int64_t>(gm) * args.ldy + gn;
+        if (gn + 32 <= args.N && args.vec_y) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 t4 = __ldg(reinterpret_cast<const float4*>(yrow + j));
+            yv[j] = t4.x; yv[j + 1] = t4.y; yv[j + 2] = t4.z; yv[j + 3] = t4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) yv[j] = (gn + j < args.N) ? __ldg(yrow + j) : 0.f;
+        }
+      };
+      auto column_chunk = [&](int c, uint32_t (&r)[32], const float (&yv)[32]) {
         const int gn = tn * BN + c * 32;
         const bool active = row_ok && gn < args.N;
         const bool full_chunk = gn + 32 <= args.N;
@@ -590,11 +607,20 @@ __global__ void __launch_bounds__(256, 1)
           }
         } else if constexpr (EPI == EPI_BIAS_RELU) {
           if (active) {
-            float v[32];
+            float v[32], bv[32];
+            if (full_chunk && args.vec_bias) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + gn + j));
+                bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) bv[j] = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
+            }
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const float bj = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
-              const float z = __fadd_rn(u32_as_f32(r[j]), bj);
+              const float z = __fadd_rn(u32_as_f32(r[j]), bv[j]);
               v[j] = (z < 0.f) ? 0.f : z;  // Relu; NaN propagates (non-finite guard)
             }
             if (args.out_f32 != nullptr) {
@@ -650,27 +676,24 @@ __global__ void __launch_bounds__(256, 1)
                   if (gn + j < args.N) v[j] = (static_cast<float>(mrow[j]) > 0.f) ? u32_as_f32(r[j]) : 0.f;
               }
             } else {  // EPI_BIAS_RELU_LOSS: a = relu(acc + b); loss seed (reading A2, A10, A20)
-              const float* yrow = args.y + static_cast<int64_t>(gm) * args.ldy + gn;
               float* o32 = args.out_f32 ? args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn : nullptr;
-              // issue all 32 target loads up front (vectorised when aligned)
-              float yv[32];
-              if (args.loss_kind == 0) {
-                if (full_chunk && args.vec_y) {
+              float bv[32];
+              if (full_chunk && args.vec_bias) {
 #pragma unroll
-                  for (int j = 0; j < 32; j += 4) {
-                    const float4 t4 = __ldg(reinterpret_cast<const float4*>(yrow + j));
-                    yv[j] = t4.x; yv[j + 1] = t4.y; yv[j + 2] = t4.z; yv[j + 3] = t4.w;
-                  }
-                } else {
-#pragma unroll
-                  for (int j = 0; j < 32; ++j) yv[j] = (gn + j < args.N) ? __ldg(yrow + j) : 0.f;
+                for (int j = 0; j < 32; j += 4) {
+                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + gn + j));
+                  bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
                 }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) bv[j] = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
               }
+              float av[32];
               float part = 0.f;  // this chunk's loss contribution (fp32), folded into loss_acc (fp64)
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
                 const bool in = gn + j < args.N;
-                const float z = __fadd_rn(u32_as_f32(r[j]), in ? __ldg(args.bias + gn + j) : 0.f);
+                const float z = __fadd_rn(u32_as_f32(r[j]), bv[j]);
                 const float a = (z < 0.f) ? 0.f : z;
                 float g;
                 if (args.loss_kind == 0) {  // MSE: d = a - y, g = d / (rows*cols) (IEEE, reading A20)
@@ -681,7 +704,7 @@ __global__ void __launch_bounds__(256, 1)
                   part = in ? __fadd_rn(part, a) : part;
                   g = args.seed_const;
                 }
-                yv[j] = a;
+                av[j] = a;
                 v[j] = (in && a > 0.f) ? g : 0.f;
               }
               loss_acc += static_cast<double>(part);
@@ -689,11 +712,11 @@ __global__ void __launch_bounds__(256, 1)
                 if (full_chunk && args.vec_out32) {
 #pragma unroll
                   for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4*>(o32 + j) = make_float4(yv[j], yv[j + 1], yv[j + 2], yv[j + 3]);
+                    *reinterpret_cast<float4*>(o32 + j) = make_float4(av[j], av[j + 1], av[j + 2], av[j + 3]);
                 } else {
 #pragma unroll
                   for (int j = 0; j < 32; ++j)
-                    if (gn + j < args.N) o32[j] = yv[j];
+                    if (gn + j < args.N) o32[j] = av[j];
                 }
               }
             }
@@ -720,17 +743,18 @@ __global__ void __launch_bounds__(256, 1)
         __syncwarp();
       };
       if constexpr (TF32) {
+        // (the K-chunk sums already hold 128 registers: one target buffer, loaded per chunk)
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
+          float yv[32];
+          if constexpr (EPI == EPI_BIAS_RELU_LOSS) load_y(c, yv);
           uint32_t r[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(kacc[c * 32 + j]);
-          column_chunk(c, r);
+          column_chunk(c, r, yv);
         }
       } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-          uint32_t r[32];
+        auto tmem_chunk = [&](int c, uint32_t (&r)[32]) {
           if (num_kb > 0) {
             ptx::tmem_ld_32x32b_x32(tmem_row + acc * BN + c * 32, r);
             ptx::tmem_ld_wait();
@@ -738,7 +762,29 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = 0u;  // K == 0: the empty sum
           }
-          column_chunk(c, r);
+        };
+        if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
+          // rolled (an unrolled epilogue overflows the instruction cache); the next chunk's
+          // targets are in flight while this chunk is processed
+          float ycur[32], ynext[32];
+          load_y(0, ycur);
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            if (c + 1 < BN / 32) load_y(c + 1, ynext);
+            uint32_t r[32];
+            tmem_chunk(c, r);
+            column_chunk(c, r, ycur);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) ycur[j] = ynext[j];
+          }
+        } else {
+          float ydummy[1][32];
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            uint32_t r[32];
+            tmem_chunk(c, r);
+            column_chunk(c, r, ydummy[0]);
+          }
         }
         if (num_kb > 0) release_tmem();
       }

@@ -45,6 +45,7 @@ struct GemmArgs {
   float inv_denom;        // 1 / loss_denom, exact when denom_pow2
   int denom_pow2;         // 1: loss_denom is a power of two, so d * inv_denom == d / loss_denom
   int vec_y;              // 1: 16-byte vector loads are aligned for y
+  int vec_bias;           // 1: 16-byte vector loads are aligned for bias
   int group_m;            // tile raster: M-tiles per group (L2 reuse of the B panels)
   int prefetch;           // k-blocks the producer's L2 prefetch runs ahead of its loads (0: off)
   int debug;              // profiling only (DFLOW_GEMM_DEBUG): 1 no TMA loads, 2 no epilogue work,
