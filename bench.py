@@ -284,7 +284,7 @@ def run_gpu(args, w):
     hptrs = D.ptr_array([Xh.data_ptr(), Yh.data_ptr()])
     hl = C.c_float(0)
     D.check(D.dflow_train_step_host(s, 2, feeds, hptrs, lds, b, C.byref(hl), sp))
-    e2e_steps = max(3, min(args.steps, 5))
+    e2e_steps = max(3, min(args.steps, 10))
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):

@@ -156,12 +156,19 @@ dflow_status dflow_variable_read(dflow_session* s, dflow_node var, void* dst, in
  * shard: forward, gradient graph, compressed exchange, update.  feeds[i] is a
  * Placeholder; dev_ptrs[i] its device data (fp32 or bf16 per the placeholder's
  * dtype) [local_rows, ld[i]], borrowed and stream-ordered on `stream`.
- * local_rows = B / N.  loss_out (host) receives C = mean_r C_r after an internal
- * sync; NULL = no host sync.                                                  */
+ * local_rows = B / N.  loss_out (host) receives C = mean_r C_r: the call waits
+ * only until the forward has produced it (Fig. 1: C is a
+ * forward node of the graph, fetched by s.run);
+ * the backward, exchange and update stay enqueued on `stream` and complete in
+ * stream order (later work on `stream` sees the updated weights).  The feeds are
+ * not read after the forward.  NULL = no host wait at all.                    */
 dflow_status dflow_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* dev_ptrs,
                               const int64_t* ld, int64_t local_rows, float* loss_out, void* stream);
 /* Same, with HOST feed buffers (pinned for async copies): copies in, steps, and
- * reads the loss back — the end-to-end path.                                  */
+ * reads the loss back — the end-to-end path.  The upload runs on the session's
+ * own copy stream, ordered after the previous step's forward (the last reader of
+ * the staging buffers), so step i+1's upload overlaps step i's backward when the
+ * caller loops.  host_ptrs may be reused as soon as the call returns.          */
 dflow_status dflow_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                    const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
                                    float* loss_out, void* stream);

@@ -311,6 +311,12 @@ dflow_status alloc_state(dflow_session* s) {
     cudaEventCreateWithFlags(&s->ev_apply[l], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&s->ev_loss, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_loss_ready, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_h2d_y, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_feeds_free, cudaEventDisableTiming);
+  if (cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(DFLOW_CUDA, "stream creation failed");
   return DFLOW_OK;
 }
 
@@ -582,6 +588,10 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
     GemmPlan& p = (mode == FWD_TRAIN) ? last.fwd : last.fwd_fetch;
     p.args.y = f.y;
     p.args.ldy = f.ldy;
+    if (s->y_upload_pending) {  // host-fed y still uploading under layers 1..L-1
+      CU(cudaStreamWaitEvent(st, s->ev_h2d_y, 0));
+      s->y_upload_pending = false;
+    }
     ST(launch_gemm(s, p, st));
     const int t = tbegin(s, 1, st);
     cudaError_t e2 = launch_loss_final(s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1, s->loss_partials, p.grid * 4, rows,
@@ -702,21 +712,32 @@ dflow_status finish_timing(dflow_session* s, cudaStream_t st) {
   return DFLOW_OK;
 }
 
-dflow_status read_loss(dflow_session* s, float* loss_out, cudaStream_t st) {
-  if (!loss_out) return DFLOW_OK;
+// The loss is final when the forward ends (k_loss_final): its device->host copy is
+// enqueued right after the forward and waited for after the backward has been enqueued,
+// so the host returns while the backward and the update still run (stream-ordered).
+dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
   if (s->opt.world > 1) {
     CU(cudaEventRecord(s->ev_loss, st));
     CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
     NC(ncclAllReduce(s->loss_dev, s->loss_dev + 1, 1, ncclFloat32, ncclSum, s->nccl, s->comm));
     CU(cudaMemcpyAsync(s->loss_host, s->loss_dev + 1, sizeof(float), cudaMemcpyDeviceToHost, s->comm));
-    CU(cudaStreamSynchronize(s->comm));
-    *loss_out = s->loss_host[0] / static_cast<float>(s->opt.world);
+    CU(cudaEventRecord(s->ev_loss_ready, s->comm));
   } else {
     CU(cudaMemcpyAsync(s->loss_host, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    *loss_out = s->loss_host[0];
+    CU(cudaEventRecord(s->ev_loss_ready, st));
   }
-  s->nonfinite = std::isfinite(*loss_out) ? 0 : 1;
+  s->loss_pending = true;
+  return DFLOW_OK;
+}
+
+dflow_status wait_loss(dflow_session* s, float* loss_out) {
+  if (!s->loss_pending) return DFLOW_OK;
+  s->loss_pending = false;
+  CU(cudaEventSynchronize(s->ev_loss_ready));
+  float v = s->loss_host[0];
+  if (s->opt.world > 1) v /= static_cast<float>(s->opt.world);
+  if (loss_out) *loss_out = v;
+  s->nonfinite = std::isfinite(v) ? 0 : 1;
   return DFLOW_OK;
 }
 
@@ -816,6 +837,9 @@ void session_destroy(dflow_session* s) {
   for (cudaEvent_t e : s->ev_apply) cudaEventDestroy(e);
   for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
   if (s->ev_loss) cudaEventDestroy(s->ev_loss);
+  for (cudaEvent_t e : {s->ev_loss_ready, s->ev_h2d, s->ev_h2d_y, s->ev_feeds_free})
+    if (e) cudaEventDestroy(e);
+  if (s->h2d) cudaStreamDestroy(s->h2d);
   if (s->comm) cudaStreamDestroy(s->comm);
   cudaGetLastError();
   delete s;
@@ -830,11 +854,13 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   s->launches = s->gemm_launches = 0;
   s->epoch++;  // p2p exchange flags of this step
   ST(run_forward(s, f, rows, st, FWD_TRAIN));
+  CU(cudaEventRecord(s->ev_feeds_free, st));  // x and y are not read after the forward
+  if (loss_out) ST(enqueue_loss(s, st));
   ST(run_backward(s, rows, st, 0));
   CU(cudaGetLastError());
   s->last_launches = s->launches;
   s->last_gemm_launches = s->gemm_launches;
-  ST(read_loss(s, loss_out, st));
+  ST(wait_loss(s, loss_out));
   if (s->timing) {
     ST(finish_timing(s, st));
     s->timed_steps++;
@@ -849,23 +875,37 @@ dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_
   if (n_feeds < 0 || n_feeds > 2 || (n_feeds > 0 && (!feeds || !host_ptrs || !ld)))
     return fail(DFLOW_INVALID_ARGUMENT, "bad feed arrays");
   const void* dptrs[2];
+  int sids[2] = {-1, -1};
   for (int i = 0; i < n_feeds; ++i) {
-    const int sid = (feeds[i] >= 0 && feeds[i] < (int)s->remap.size()) ? s->remap[feeds[i]] : -1;
-    if (sid < 0) return fail(DFLOW_INVALID_ARGUMENT, "bad feed node");
-    const size_t esz = (sid == s->x && s->x_dtype == DFLOW_BF16) ? 2 : 4;
-    const size_t bytes = static_cast<size_t>(rows) * ld[i] * esz;
-    if (s->host_stage_bytes[i] < bytes) {
-      if (s->host_stage[i]) cudaFree(s->host_stage[i]);
-      s->host_stage[i] = nullptr;
-      if (cudaMalloc(&s->host_stage[i], bytes) != cudaSuccess) return fail(DFLOW_OOM, "staging buffer");
-      s->host_stage_bytes[i] = bytes;
-    }
-    CU(cudaMemcpyAsync(s->host_stage[i], host_ptrs[i], bytes, cudaMemcpyHostToDevice, st));
-    dptrs[i] = s->host_stage[i];
+    sids[i] = (feeds[i] >= 0 && feeds[i] < (int)s->remap.size()) ? s->remap[feeds[i]] : -1;
+    if (sids[i] < 0) return fail(DFLOW_INVALID_ARGUMENT, "bad feed node");
   }
+  CU(cudaStreamWaitEvent(s->h2d, s->ev_feeds_free, 0));  // the previous forward is done with them
+  // x first, then y (its upload overlaps the first layers of the forward)
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i < n_feeds; ++i) {
+      if ((sids[i] == s->y) != (pass == 1)) continue;
+      const size_t esz = (sids[i] == s->x && s->x_dtype == DFLOW_BF16) ? 2 : 4;
+      const size_t bytes = static_cast<size_t>(rows) * ld[i] * esz;
+      if (s->host_stage_bytes[i] < bytes) {
+        if (s->host_stage[i]) cudaFree(s->host_stage[i]);
+        s->host_stage[i] = nullptr;
+        if (cudaMalloc(&s->host_stage[i], bytes) != cudaSuccess) return fail(DFLOW_OOM, "staging buffer");
+        s->host_stage_bytes[i] = bytes;
+      }
+      CU(cudaMemcpyAsync(s->host_stage[i], host_ptrs[i], bytes, cudaMemcpyHostToDevice, s->h2d));
+      dptrs[i] = s->host_stage[i];
+    }
+    CU(cudaEventRecord(pass == 0 ? s->ev_h2d : s->ev_h2d_y, s->h2d));
+  }
+  CU(cudaStreamWaitEvent(st, s->ev_h2d, 0));
+  s->y_upload_pending = true;
   float loss = 0.f;
-  ST(session_train_step(s, n_feeds, feeds, dptrs, ld, rows, &loss, st));
+  const dflow_status r = session_train_step(s, n_feeds, feeds, dptrs, ld, rows, &loss, st);
+  s->y_upload_pending = false;
+  if (r != DFLOW_OK) return r;
   if (loss_out) *loss_out = loss;
+  else CU(cudaEventSynchronize(s->ev_h2d_y));  // host_ptrs are reusable on return
   return DFLOW_OK;
 }
 

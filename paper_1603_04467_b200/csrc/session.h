@@ -90,6 +90,15 @@ struct dflow_session {
   cudaStream_t comm = nullptr;
   std::vector<cudaEvent_t> ev_grad, ev_apply;
   cudaEvent_t ev_loss = nullptr;
+  cudaEvent_t ev_loss_ready = nullptr;  // loss value landed in loss_host (after the forward)
+  bool loss_pending = false;
+  // e2e path: host feeds are copied on their own stream so step i+1's upload overlaps
+  // step i's backward; ev_feeds_free marks the forward done reading the staging buffers
+  // (x is uploaded first; y, needed only by the last layer's loss epilogue, uploads while
+  // the first layers run: the step's forward waits on ev_h2d, its last GEMM on ev_h2d_y)
+  cudaStream_t h2d = nullptr;
+  cudaEvent_t ev_h2d = nullptr, ev_h2d_y = nullptr, ev_feeds_free = nullptr;
+  bool y_upload_pending = false;
   ncclComm_t nccl = nullptr;
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;

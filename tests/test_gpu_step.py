@@ -12,7 +12,10 @@ pytestmark = pytest.mark.gpu
 
 from oracle.mlp import build_mlp, forward, train_step  # noqa: E402
 from synth import C1, C1_BIAS, C2, C3, batch, exact_regime, init_params, with_batch  # noqa: E402
-from dflow_harness import Run, normwise  # noqa: E402
+import ctypes as C  # noqa: E402
+
+import paper_1603_04467_b200 as D  # noqa: E402
+from dflow_harness import Run, normwise, stream_ptr  # noqa: E402
 
 BF16_TOL = 2e-2
 
@@ -167,3 +170,32 @@ def test_p16_hundred_steps_config2():
         assert losses_g[-1] < losses_g[0]
     finally:
         run.close()
+
+
+def test_host_fed_steps_match_device_fed_bitwise():
+    # dflow_train_step_host: x uploads first, y under the first layers, step i+1's upload under
+    # step i's backward; the result must be the device-fed step's, bit for bit, every step
+    w = with_batch(C2, 512)
+    Ws, bs = init_params(w)
+    dev = Run(w.dims, "MSE", w.lr, rows=w.batch)
+    host = Run(w.dims, "MSE", w.lr, rows=w.batch)
+    try:
+        dev.assign(Ws, bs)
+        host.assign(Ws, bs)
+        ids, lds = D.node_array([host.mlp.x, host.mlp.y]), D.i64_array([w.dims[0], w.dims[-1]])
+        for step in range(4):
+            X, Y = batch(w, step=step)
+            ld = dev.step(_dev(X), _dev(Y))
+            Xh, Yh = torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory()
+            lh = C.c_float(0)
+            D.check(D.dflow_train_step_host(host.s, 2, ids, D.ptr_array([Xh.data_ptr(), Yh.data_ptr()]), lds,
+                                            w.batch, C.byref(lh) if step % 2 == 0 else None, stream_ptr()))
+            if step % 2 == 0:
+                assert np.float32(lh.value).view(np.uint32) == np.float32(ld).view(np.uint32), step
+        Wd, bd = dev.read()
+        Wh, bh = host.read()
+        for a, b in zip(Wd + bd, Wh + bh):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    finally:
+        dev.close()
+        host.close()
