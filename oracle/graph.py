@@ -35,7 +35,9 @@ INVALID_ARGUMENT = "INVALID_ARGUMENT"
 OPS = ("Placeholder", "Variable", "MatMul", "Add", "Relu", "Loss", "LossGrad", "ReluGrad",
        "ReduceSum", "AddN", "ZerosLike", "ApplyGradientDescent",
        # inserted by insert_exchange (the replicated graph's transfer nodes)
-       "Truncate16", "CrossReplicaMeanT16", "Expand16", "CrossReplicaMean")
+       "Truncate16", "CrossReplicaMeanT16", "Expand16", "CrossReplicaMean",
+       # f2: the probabilistic-rounding variant of the same channel (reading A26)
+       "StochasticRound16", "CrossReplicaMeanSR16")
 BATCH = -1  # unknown (batch) dimension, only allowed through Placeholder
 _NAME_RE = re.compile(r"^[A-Za-z0-9_./]+$")
 
@@ -275,7 +277,8 @@ def insert_exchange(graph: Graph, world: int, exchange: str) -> Graph:
     """Compression-insertion on the replica->combine transfer (PAPER.md :813-821 on the
     §7 :934-941 channel; SPEC.md:681-689 shape).  For world > 1, between every
     ApplyGradientDescent and its gradient: TRUNC16 -> Truncate16, CrossReplicaMeanT16
-    (attr world), Expand16; FP32 modes -> CrossReplicaMean.  world == 1 or NONE: a copy
+    (attr world), Expand16; SR16 -> StochasticRound16, CrossReplicaMeanSR16, Expand16;
+    FP32 modes -> CrossReplicaMean.  world == 1 or NONE: a copy
     (reading A6).  The replicas themselves are implicit (one per rank)."""
     out = Graph()
     active = world > 1 and exchange != "NONE"
@@ -287,6 +290,10 @@ def insert_exchange(graph: Graph, world: int, exchange: str) -> Graph:
             if exchange == "TRUNC16":
                 t = out._add(f"xchg/{var}/trunc16", "Truncate16", [g], {}, "u16", G.shape)
                 m = out._add(f"xchg/{var}/mean", "CrossReplicaMeanT16", [t], {"world": world}, "u16", G.shape)
+                inputs[1] = out._add(f"xchg/{var}/expand16", "Expand16", [m], {}, "f32", G.shape)
+            elif exchange == "SR16":
+                t = out._add(f"xchg/{var}/sround16", "StochasticRound16", [g], {}, "u16", G.shape)
+                m = out._add(f"xchg/{var}/mean", "CrossReplicaMeanSR16", [t], {"world": world}, "u16", G.shape)
                 inputs[1] = out._add(f"xchg/{var}/expand16", "Expand16", [m], {}, "f32", G.shape)
             else:
                 inputs[1] = out._add(f"xchg/{var}/mean", "CrossReplicaMean", [g], {"world": world}, "f32", G.shape)

@@ -123,10 +123,13 @@ def replica_gradients(mg: MLPGraph, Ws, bs, X, Y=None, mode: str = "f32",
 
 
 def train_step(mg: MLPGraph, Ws, bs, X, Y=None, n_replicas: int = 1, exchange: str = "TRUNC16",
-               mode: str = "f32", masks: Optional[Sequence[Dict[str, np.ndarray]]] = None) -> dict:
+               mode: str = "f32", masks: Optional[Sequence[Dict[str, np.ndarray]]] = None,
+               sr_seed: int = 0, step: int = 1) -> dict:
     """One synchronous replicated SGD step.  Returns W/b after the step, the
     mean cost, per-replica gradients, the combined g_hat, and (when ``masks``
-    is given: mask-locked mode) the number of Relu mask flips per layer."""
+    is given: mask-locked mode) the number of Relu mask flips per layer.
+    SR16 combines each layer's bucket [dW_l ; db_l] (reading A28) with the
+    stochastic-rounding streams of (sr_seed, step, layer)."""
     B = X.shape[0]
     if B % n_replicas:
         raise GraphError(INVALID_ARGUMENT, f"batch {B} not divisible by {n_replicas} replicas")
@@ -145,7 +148,17 @@ def train_step(mg: MLPGraph, Ws, bs, X, Y=None, n_replicas: int = 1, exchange: s
         per.append(res)
     variables = _variables(mg, Ws, bs, mode)
     ghat = {}
+    if exchange == "SR16" and n_replicas > 1 and mode != "f64":
+        for l, (wv, bv) in enumerate(zip(mg.weights, mg.biases)):
+            gs = [np.concatenate([p[wv].ravel(), p[bv].ravel()]).astype(np.float32) for p in per]
+            g = combine(gs, "SR16", sr=(sr_seed, step, l))
+            nw = per[0][wv].size
+            ghat[wv] = g[:nw].reshape(per[0][wv].shape)
+            ghat[bv] = g[nw:].reshape(per[0][bv].shape)
     for v in mg.weights + mg.biases:
+        if v in ghat:
+            variables[v] = K.apply_gradient_descent(variables[v], mg.lr, ghat[v], mode)
+            continue
         gs = [p[v] for p in per]
         if mode == "f64":
             if exchange not in ("FP32",) and n_replicas > 1:
