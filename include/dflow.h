@@ -122,6 +122,9 @@ dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int ex
 #define DFLOW_EXCHANGE_FP32 1     /* same schedule with fp32 payloads (deterministic)              */
 #define DFLOW_EXCHANGE_FP32_NCCL 2 /* ncclAllReduce(sum, fp32) then x 1/N (library baseline)        */
 #define DFLOW_EXCHANGE_NONE 3     /* debug/timing only: no exchange (N>1 results are wrong)        */
+#define DFLOW_EXCHANGE_SR16 4     /* TRUNC16's schedule with both 32->16 codings done by stochastic
+                                     rounding (f2; "probabilistic rounding";
+                                     readings A26-A28; draws keyed by options.sr_seed)           */
 
 typedef struct {
   int32_t world;          /* N replicas (one process or thread per GPU)                      */
@@ -135,6 +138,7 @@ typedef struct {
   int32_t p2p;            /* TRUNC16, N > 1: 1 = fused NVLink exchange (the dW epilogue stores the
                              truncated tiles into the owners' buffers through CUDA IPC peer
                              pointers; owner fold + all-gather by peer stores); 0 = NCCL calls  */
+  uint32_t sr_seed;       /* SR16: seed of the counter-based draw streams (reading A27)        */
 } dflow_options;
 
 /* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */
@@ -205,6 +209,17 @@ dflow_status dflow_session_stats(dflow_session* s, dflow_stats* out);
  * Bit-exact codec (reading A5): dst[i] = bits(src[i]) >> 16,
  * and dst[i] = float(bits = src[i] << 16).  Device pointers, n elements.       */
 dflow_status dflow_truncate16(const float* src, uint16_t* dst, size_t n, void* stream);
+/* a6 with either coding, on one device buffer: dst[i] = 16-bit code of src[i] at bucket
+ * position idx_base + i — (bits + r) >> 16 with r = mix32((idx) ^ key) >> 16 when
+ * stochastic (SR16, readings A26-A27), else bits >> 16.  Stream-ordered.        */
+dflow_status dflow_round16(const float* src, uint16_t* dst, size_t n, uint32_t key, int stochastic, int64_t idx_base,
+                           void* stream);
+/* The SR16 stream key of one compression point (reading A27): stage 0 = a sender's
+ * coding of its gradient, stage 1 = the owner's coding of the mean; step = the
+ * session's 1-based step (train steps and standalone exchanges count separately,
+ * see dflow_exchange); layer = bucket id (0-based layer; 0 for dflow_exchange).    */
+dflow_status dflow_round16_key(uint32_t seed, uint32_t step, uint32_t layer, uint32_t stage, uint32_t rank,
+                               uint32_t* key_out);
 dflow_status dflow_expand16(const uint16_t* src, float* dst, size_t n, void* stream);
 /* Exchange alone (a6-a8) on this session's communicator: grad_dev fp32 [n] on
  * every rank -> out_dev fp32 [n] = the g_hat every replica applies.           */

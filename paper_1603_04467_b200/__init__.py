@@ -35,14 +35,15 @@ DFLOW_BATCH = -1
 DFLOW_LOSS_MSE, DFLOW_LOSS_SUM = 0, 1
 DFLOW_PRECISION_BF16, DFLOW_PRECISION_3XTF32 = 0, 1
 DFLOW_EXCHANGE_TRUNC16, DFLOW_EXCHANGE_FP32, DFLOW_EXCHANGE_FP32_NCCL, DFLOW_EXCHANGE_NONE = 0, 1, 2, 3
-EXCHANGES = {"TRUNC16": 0, "FP32": 1, "FP32_NCCL": 2, "NONE": 3}
+DFLOW_EXCHANGE_SR16 = 4
+EXCHANGES = {"TRUNC16": 0, "FP32": 1, "FP32_NCCL": 2, "NONE": 3, "SR16": 4}
 EPI_F32, EPI_TRUNC16, EPI_BIAS_RELU, EPI_RELUGRAD = 0, 1, 2, 3
 
 
 class dflow_options(C.Structure):
     _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32), ("precision", C.c_int32),
                 ("exchange", C.c_int32), ("overlap", C.c_int32), ("sm_reserve", C.c_int32),
-                ("max_local_rows", C.c_int64), ("p2p", C.c_int32)]
+                ("max_local_rows", C.c_int64), ("p2p", C.c_int32), ("sr_seed", C.c_uint32)]
 
 
 class dflow_stats(C.Structure):
@@ -89,6 +90,9 @@ _SIGS = {
     "dflow_session_set_timing": (_i32, [_p, _i32]),
     "dflow_session_stats": (_i32, [_p, C.POINTER(dflow_stats)]),
     "dflow_truncate16": (_i32, [_p, _p, _sz, _p]),
+    "dflow_round16": (_i32, [_p, _p, _sz, C.c_uint32, C.c_int, C.c_int64, _p]),
+    "dflow_round16_key": (_i32, [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.POINTER(C.c_uint32)]),
     "dflow_expand16": (_i32, [_p, _p, _sz, _p]),
     "dflow_exchange": (_i32, [_p, _p, _p, _sz, _p]),
     "dflow_gemm_bf16": (_i32, [_i64, _i64, _i64, _p, _i64, _i32, _p, _i64, _i32, _i32, _p, _i64, _p, _i64, _p, _p,
@@ -215,9 +219,9 @@ def _node_name(g, nid) -> bytes:
 
 
 def make_options(world=1, rank=0, device=0, precision=DFLOW_PRECISION_BF16, exchange="TRUNC16", overlap=1,
-                 sm_reserve=0, max_local_rows=1, p2p=0) -> dflow_options:
+                 sm_reserve=0, max_local_rows=1, p2p=0, sr_seed=0) -> dflow_options:
     ex = EXCHANGES[exchange] if isinstance(exchange, str) else int(exchange)
-    return dflow_options(world, rank, device, precision, ex, overlap, sm_reserve, max_local_rows, p2p)
+    return dflow_options(world, rank, device, precision, ex, overlap, sm_reserve, max_local_rows, p2p, sr_seed)
 
 
 def session_create(mlp_or_graph, opts: dflow_options, nccl_id: bytes = None):

@@ -184,7 +184,7 @@ dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, si
 dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int exchange, dflow_graph** out) {
   GUARD_BEGIN
   if (!g || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
-  if (world < 1 || exchange < DFLOW_EXCHANGE_TRUNC16 || exchange > DFLOW_EXCHANGE_NONE)
+  if (world < 1 || exchange < DFLOW_EXCHANGE_TRUNC16 || exchange > DFLOW_EXCHANGE_SR16)
     return fail(DFLOW_INVALID_ARGUMENT, "bad world/exchange");
   dflow_graph* r = new dflow_graph();
   std::vector<int> remap;
@@ -309,6 +309,23 @@ dflow_status dflow_truncate16(const float* src, uint16_t* dst, size_t n, void* s
   if (n && (!src || !dst)) return fail(DFLOW_INVALID_ARGUMENT, "NULL pointer");
   cudaError_t e = dflow::launch_truncate16(src, dst, n, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(DFLOW_CUDA, "truncate16: %s", cudaGetErrorString(e));
+  return DFLOW_OK;
+}
+
+dflow_status dflow_round16(const float* src, uint16_t* dst, size_t n, uint32_t key, int stochastic, int64_t idx_base,
+                           void* stream) {
+  if (n && (!src || !dst)) return fail(DFLOW_INVALID_ARGUMENT, "NULL pointer");
+  if (idx_base < 0) return fail(DFLOW_INVALID_ARGUMENT, "negative idx_base");
+  cudaError_t e = dflow::launch_round16(src, dst, n, dflow::Round16{key, stochastic ? 1 : 0}, idx_base,
+                                        static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(DFLOW_CUDA, "round16: %s", cudaGetErrorString(e));
+  return DFLOW_OK;
+}
+
+dflow_status dflow_round16_key(uint32_t seed, uint32_t step, uint32_t layer, uint32_t stage, uint32_t rank,
+                               uint32_t* key_out) {
+  if (!key_out) return fail(DFLOW_INVALID_ARGUMENT, "NULL key_out");
+  *key_out = dflow::round16_key(seed, step, layer, stage, rank);
   return DFLOW_OK;
 }
 

@@ -28,6 +28,8 @@ const char* op_name(Op op) {
     case Op::CrossReplicaMeanT16: return "CrossReplicaMeanT16";
     case Op::Expand16: return "Expand16";
     case Op::CrossReplicaMean: return "CrossReplicaMean";
+    case Op::StochasticRound16: return "StochasticRound16";
+    case Op::CrossReplicaMeanSR16: return "CrossReplicaMeanSR16";
   }
   return "?";
 }
@@ -395,6 +397,7 @@ std::string Graph::to_json() const {
         break;
       case Op::CrossReplicaMean:
       case Op::CrossReplicaMeanT16:
+      case Op::CrossReplicaMeanSR16:
         snprintf(buf, sizeof buf, "\"world\": %d", n.world);
         o += buf;
         break;
@@ -438,17 +441,18 @@ dflow_status insert_exchange(const Graph& in, int world, int exchange, Graph* ou
       const Node gnode = out->nodes[g];
       int id;
       dflow_status st;
-      if (exchange == DFLOW_EXCHANGE_TRUNC16) {
+      if (exchange == DFLOW_EXCHANGE_TRUNC16 || exchange == DFLOW_EXCHANGE_SR16) {
+        const bool sr = exchange == DFLOW_EXCHANGE_SR16;
         Node t;
-        t.name = "xchg/" + var + "/trunc16";
-        t.op = Op::Truncate16;
+        t.name = "xchg/" + var + (sr ? "/sround16" : "/trunc16");
+        t.op = sr ? Op::StochasticRound16 : Op::Truncate16;
         t.inputs = {g};
         t.dtype = DFLOW_U16;
         t.shape = gnode.shape;
         if ((st = out->append(t, &id))) return st;
         Node m;
         m.name = "xchg/" + var + "/mean";
-        m.op = Op::CrossReplicaMeanT16;
+        m.op = sr ? Op::CrossReplicaMeanSR16 : Op::CrossReplicaMeanT16;
         m.inputs = {id};
         m.dtype = DFLOW_U16;
         m.shape = gnode.shape;

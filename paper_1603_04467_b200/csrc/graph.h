@@ -29,6 +29,8 @@ enum class Op : int {
   CrossReplicaMeanT16,
   Expand16,
   CrossReplicaMean,
+  StochasticRound16,     // SR16 (f2)
+  CrossReplicaMeanSR16,
 };
 
 const char* op_name(Op op);

@@ -53,6 +53,15 @@ __global__ void k_truncate16(const float* __restrict__ src, uint16_t* __restrict
   for (int64_t i = done + tid; i < n; i += stride) dst[i] = static_cast<uint16_t>(s[i] >> 16);
 }
 
+// a6 with the SR16 codec: element i is bucket position idx_base + i
+__global__ void k_round16(const float* __restrict__ src, uint16_t* __restrict__ dst, int64_t n, Round16 r,
+                          int64_t idx_base) {
+  const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = static_cast<uint16_t>(round16(s[i], idx_base + i, r));
+}
+
 __global__ void k_expand16(const uint16_t* __restrict__ src, float* __restrict__ dst, int64_t n, int vec) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -189,7 +198,7 @@ __global__ void k_loss_final(int kind, const double* __restrict__ partials, int 
 // Block = 32 columns x 8 chunk-groups; group g sums chunks g, g+8, ... in order, then
 // the 8 group sums are added in group order (deterministic, ~#chunks/8 dependent adds).
 __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols, float* __restrict__ out32,
-                               uint16_t* __restrict__ out16) {
+                               uint16_t* __restrict__ out16, Round16 r16, int64_t idx_base) {
   __shared__ float sm[8][33];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t c = blockIdx.x * 32LL + cl;
@@ -210,13 +219,13 @@ __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t
 #pragma unroll
     for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
     if (out32) out32[c] = s;
-    if (out16) out16[c] = static_cast<uint16_t>(__float_as_uint(s) >> 16);
+    if (out16) out16[c] = static_cast<uint16_t>(round16(__float_as_uint(s), idx_base + c, r16));
   }
 }
 
 // ------------------------------------------------------------------ owner reduce
 __global__ void k_owner_reduce_t16(const uint16_t* __restrict__ recv, int64_t shard, int nranks,
-                                   uint16_t* __restrict__ out) {
+                                   uint16_t* __restrict__ out, Round16 r16, int64_t idx_base) {
   const float inv = 1.0f / static_cast<float>(nranks);  // exact for power-of-two N (reading A7)
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -238,9 +247,9 @@ __global__ void k_owner_reduce_t16(const uint16_t* __restrict__ recv, int64_t sh
     uint32_t o[4];
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const uint32_t lo = __float_as_uint(__fmul_rn(s[e], inv)) >> 16;
-      const uint32_t hi = __float_as_uint(__fmul_rn(s[e + 1], inv)) & 0xFFFF0000u;
-      o[e >> 1] = lo | hi;
+      const uint32_t lo = round16(__float_as_uint(__fmul_rn(s[e], inv)), idx_base + 8 * i + e, r16);
+      const uint32_t hi = round16(__float_as_uint(__fmul_rn(s[e + 1], inv)), idx_base + 8 * i + e + 1, r16);
+      o[e >> 1] = lo | (hi << 16);
     }
     reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
@@ -361,6 +370,13 @@ cudaError_t launch_truncate16(const float* src, uint16_t* dst, size_t n, cudaStr
   return cudaGetLastError();
 }
 
+cudaError_t launch_round16(const float* src, uint16_t* dst, size_t n, Round16 r, int64_t idx_base, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  if (!r.stochastic && idx_base == 0) return launch_truncate16(src, dst, n, s);
+  k_round16<<<blocks_for((int64_t)n), kThreads, 0, s>>>(src, dst, (int64_t)n, r, idx_base);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand16(const uint16_t* src, float* dst, size_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   const int vec = al16(src) && al16(dst);
@@ -415,16 +431,17 @@ cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t r
 }
 
 cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
-                                cudaStream_t s) {
+                                cudaStream_t s, Round16 r, int64_t idx_base) {
   if (cols == 0) return cudaSuccess;
-  k_colsum_final<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16);
+  k_colsum_final<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16, r,
+                                                                          idx_base);
   return cudaGetLastError();
 }
 
 cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,
-                                    cudaStream_t s) {
+                                    cudaStream_t s, Round16 r, int64_t idx_base) {
   if (shard == 0) return cudaSuccess;
-  k_owner_reduce_t16<<<blocks_for(shard / 8), kThreads, 0, s>>>(recv, shard, nranks, out);
+  k_owner_reduce_t16<<<blocks_for(shard / 8), kThreads, 0, s>>>(recv, shard, nranks, out, r, idx_base);
   return cudaGetLastError();
 }
 

@@ -5,10 +5,14 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "round16.h"
+
 namespace dflow {
 
 // NK9 / NK10: dst[i] = bits(src[i]) >> 16  /  dst[i] = float(bits = src[i] << 16)
 cudaError_t launch_truncate16(const float* src, uint16_t* dst, size_t n, cudaStream_t s);
+// a6 with either codec (round16.h): dst[i] = round16(bits(src[i]), idx_base + i, r)
+cudaError_t launch_round16(const float* src, uint16_t* dst, size_t n, Round16 r, int64_t idx_base, cudaStream_t s);
 cudaError_t launch_expand16(const uint16_t* src, float* dst, size_t n, cudaStream_t s);
 
 // NK13: dst bf16 [rows, ldd] = RNE(src f32 [rows, lds]) for cols columns.
@@ -33,12 +37,14 @@ cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t r
 
 // NK8 final pass: db[c] = sum_k ws[k, c] over the `chunks` per-32-row partial
 // column sums the dz-producing epilogue wrote (fixed order).  fp32 and/or u16 out.
+// The u16 output is round16(bits(db[c]), idx_base + c, r) (the db tail of the layer bucket).
 cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
-                                cudaStream_t s);
+                                cudaStream_t s, Round16 r = {0, 0}, int64_t idx_base = 0);
 
-// NK11: owner fold of N received shards (rank order), x (1/N), truncate.
+// NK11: owner fold of N received shards (rank order), x (1/N), 16-bit code (truncate or
+// SR16 at bucket positions idx_base + i).
 cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,
-                                    cudaStream_t s);
+                                    cudaStream_t s, Round16 r = {0, 0}, int64_t idx_base = 0);
 cudaError_t launch_owner_reduce_f32(const float* recv, int64_t shard, int nranks, float* out, cudaStream_t s);
 // x (1/N) in place (FP32_NCCL after an allreduce-sum).
 cudaError_t launch_scale_f32(float* x, int64_t n, float scale, cudaStream_t s);

@@ -47,7 +47,7 @@ __device__ __forceinline__ void grid_signal(const P2PLayer& p, int phase, uint32
 }
 
 __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int64_t cols, int64_t base_idx,
-                                   const P2PLayer p, uint32_t epoch) {
+                                   const P2PLayer p, uint32_t epoch, Round16 r16) {
   __shared__ float sm[8][33];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t c = blockIdx.x * 32LL + cl;
@@ -70,12 +70,12 @@ __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int
     const int64_t idx = base_idx + c;
     const int owner = static_cast<int>(idx / p.shard);
     p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
-        static_cast<uint16_t>(__float_as_uint(s) >> 16);
+        static_cast<uint16_t>(round16(__float_as_uint(s), idx, r16));
   }
   grid_signal(p, 0, epoch);
 }
 
-__global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch) {
+__global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16) {
   block_wait_flags(p.flags[p.rank], p.world, epoch);  // every rank's contribution has landed
   const float inv = 1.0f / static_cast<float>(p.world);
   const uint16_t* recv = p.recv[p.rank];
@@ -96,11 +96,12 @@ __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch) {
       for (int e = 0; e < 8; ++e) s[e] = __fadd_rn(s[e], __uint_as_float((w[e >> 1] >> ((e & 1) * 16)) << 16));
     }
     uint32_t o[4];
+    const int64_t idx0 = static_cast<int64_t>(p.rank) * p.shard + 8 * i;  // bucket position of element 0
 #pragma unroll
     for (int e = 0; e < 8; e += 2) {
-      const uint32_t lo = __float_as_uint(__fmul_rn(s[e], inv)) >> 16;
-      const uint32_t hi = __float_as_uint(__fmul_rn(s[e + 1], inv)) & 0xFFFF0000u;
-      o[e >> 1] = lo | hi;
+      const uint32_t lo = round16(__float_as_uint(__fmul_rn(s[e], inv)), idx0 + e, r16);
+      const uint32_t hi = round16(__float_as_uint(__fmul_rn(s[e + 1], inv)), idx0 + e + 1, r16);
+      o[e >> 1] = lo | (hi << 16);
     }
     const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
     for (int j = 0; j < p.world; ++j)  // all-gather leg: push q_bar to every rank (NVLink stores)
@@ -117,16 +118,16 @@ __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
 }  // namespace
 
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
-                                    uint32_t epoch, cudaStream_t s) {
+                                    uint32_t epoch, cudaStream_t s, Round16 r) {
   const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 31) / 32));
-  k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch);
+  k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);
   return cudaGetLastError();
 }
 
-cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s) {
+cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s, Round16 r) {
   const int64_t nv = p.shard / 8;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((nv + 255) / 256, 148 * 2)));
-  k_owner_reduce_p2p<<<blocks, 256, 0, s>>>(p, epoch);
+  k_owner_reduce_p2p<<<blocks, 256, 0, s>>>(p, epoch, r);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "gemm.h"
+#include "round16.h"
 
 namespace dflow {
 
@@ -29,12 +30,12 @@ struct P2PLayer {
   int rank, world;
 };
 
-// db_l (sum of the per-32-row partials), truncated and stored at bucket index
+// db_l (sum of the per-32-row partials), coded (truncate / SR16) and stored at bucket index
 // base_idx + c in its owner's receive slot; then phase-0 flags.
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
-                                    uint32_t epoch, cudaStream_t s);
-// Owner step over peer memory (see above).
-cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s);
+                                    uint32_t epoch, cudaStream_t s, Round16 r = {0, 0});
+// Owner step over peer memory (see above); the mean is coded with r (truncate or SR16).
+cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s, Round16 r = {0, 0});
 // Block until all `world` phase-1 flags of this rank reach `epoch` (one CTA, acquire.sys).
 cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
 

@@ -523,20 +523,22 @@ __global__ void __launch_bounds__(256, 1)
         } else if constexpr (EPI == EPI_TRUNC16) {
           if (active) {
             uint16_t* o = reinterpret_cast<uint16_t*>(args.out) + static_cast<int64_t>(gm) * args.ldo + gn;
+            const uint64_t ib = static_cast<uint64_t>(gm) * args.N + gn;  // bucket position of column gn
+            auto code = [&](int j) { return round16(r[j], ib + j, args.r16); };
             if (full_chunk && args.vec_out) {
 #pragma unroll
               for (int j = 0; j < 32; j += 8) {
                 uint4 v;
-                v.x = (r[j] >> 16) | (r[j + 1] & 0xFFFF0000u);
-                v.y = (r[j + 2] >> 16) | (r[j + 3] & 0xFFFF0000u);
-                v.z = (r[j + 4] >> 16) | (r[j + 5] & 0xFFFF0000u);
-                v.w = (r[j + 6] >> 16) | (r[j + 7] & 0xFFFF0000u);
+                v.x = code(j) | (code(j + 1) << 16);
+                v.y = code(j + 2) | (code(j + 3) << 16);
+                v.z = code(j + 4) | (code(j + 5) << 16);
+                v.w = code(j + 6) | (code(j + 7) << 16);
                 *reinterpret_cast<uint4*>(o + j) = v;
               }
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
-                if (gn + j < args.N) o[j] = static_cast<uint16_t>(r[j] >> 16);
+                if (gn + j < args.N) o[j] = static_cast<uint16_t>(code(j));
             }
           }
         } else if constexpr (EPI == EPI_TRUNC16_P2P) {
@@ -545,8 +547,10 @@ __global__ void __launch_bounds__(256, 1)
           // 8-element groups never straddle an owner (shard % 8 == 0, N % 8 == 0 on that path)
           uint16_t* stg = stg_base + q * 32 * Cfg::STG_PITCH;
           uint32_t* srow = reinterpret_cast<uint32_t*>(stg + lane * Cfg::STG_PITCH + (c & 1) * 32);
+          const uint64_t ib = static_cast<uint64_t>(gm) * args.N + gn;  // bucket position of column gn
 #pragma unroll
-          for (int j = 0; j < 16; ++j) srow[j] = (r[2 * j] >> 16) | (r[2 * j + 1] & 0xFFFF0000u);
+          for (int j = 0; j < 16; ++j)
+            srow[j] = round16(r[2 * j], ib + 2 * j, args.r16) | (round16(r[2 * j + 1], ib + 2 * j + 1, args.r16) << 16);
           if (c & 1) {
             __syncwarp();
             const int gm0 = tm * (BM * CG) + cta_rank * BM + q * 32;

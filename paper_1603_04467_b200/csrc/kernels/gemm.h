@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "round16.h"
+
 namespace dflow {
 
 // "operand" outputs are written as bf16 (RNE) in the bf16 path, or as the tf32
@@ -62,6 +64,9 @@ struct GemmArgs {
   int64_t p2p_shard;
   int p2p_rank;
   int p2p_world;
+  // EPI_TRUNC16 / EPI_TRUNC16_P2P: the 16-bit code of element (m, n) is
+  // round16(bits, m*N + n, r16) — truncation, or SR16 (reading A26)
+  Round16 r16;
 };
 
 struct GemmDesc {

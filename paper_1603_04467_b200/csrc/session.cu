@@ -51,6 +51,20 @@ namespace {
 
 inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// Gradients cross the channel as 16-bit codes (TRUNC16 or SR16).
+inline bool u16_wire(const dflow_session* s) {
+  return s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 || s->opt.exchange == DFLOW_EXCHANGE_SR16;
+}
+
+// The coding of layer l's bucket at compression point `stage` (0: this rank as sender,
+// 1: this rank as owner of the mean) in the current train step (epoch, 1-based).
+inline Round16 round16_of(const dflow_session* s, int l, int stage) {
+  if (s->opt.exchange != DFLOW_EXCHANGE_SR16) return Round16{0, 0};
+  return Round16{round16_key(s->opt.sr_seed, s->epoch, static_cast<uint32_t>(l), static_cast<uint32_t>(stage),
+                             static_cast<uint32_t>(s->opt.rank)),
+                 1};
+}
+
 int find_node(const Graph& g, Op op, const std::vector<int>& inputs, int ta = -1, int tb = -1) {
   for (size_t i = 0; i < g.nodes.size(); ++i) {
     const Node& n = g.nodes[i];
@@ -165,13 +179,16 @@ dflow_status match_graph(dflow_session* s) {
     if (ap.op != Op::ApplyGradientDescent) continue;
     int gid = ap.inputs[1];
     std::vector<int> chain;
-    if (xchg && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+    if (xchg && u16_wire(s)) {
+      const bool sr = s->opt.exchange == DFLOW_EXCHANGE_SR16;
       const int e = gid;
       if (g.nodes[e].op != Op::Expand16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing Expand16 before apply");
       const int m = g.nodes[e].inputs[0];
-      if (g.nodes[m].op != Op::CrossReplicaMeanT16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
+      if (g.nodes[m].op != (sr ? Op::CrossReplicaMeanSR16 : Op::CrossReplicaMeanT16))
+        return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
       const int t = g.nodes[m].inputs[0];
-      if (g.nodes[t].op != Op::Truncate16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing Truncate16");
+      if (g.nodes[t].op != (sr ? Op::StochasticRound16 : Op::Truncate16))
+        return fail(DFLOW_UNIMPLEMENTED, "planner: missing the 32->16 coding node");
       chain = {e, m, t};
       gid = g.nodes[t].inputs[0];
     } else if (xchg) {
@@ -274,7 +291,7 @@ dflow_status alloc_state(dflow_session* s) {
     ly.shard = ly.Ppad / N;
     ST(dmalloc(s, &ly.g32, ly.Ppad));
     ST(dmalloc(s, &ly.colsum_ws, ((cap + 31) / 32) * ly.out));
-    if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 && !s->p2p) {
+    if (N > 1 && u16_wire(s) && !s->p2p) {
       ST(dmalloc(s, &ly.q16, ly.Ppad));
       uint16_t *r, *o, *gt;
       ST(dmalloc(s, &r, ly.Ppad));
@@ -458,7 +475,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       ST(gemm_plan(s, wa, &ly.wgrad_apply));
       ly.has_wgrad_apply = true;
     }
-    if (s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 && !s->p2p) {
+    if (s->opt.world > 1 && u16_wire(s) && !s->p2p) {
       w.epilogue = EPI_TRUNC16;
       w.out_f32 = nullptr;
       w.out = ly.q16; w.out2 = nullptr; w.ldo = ly.out;
@@ -617,12 +634,14 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
     CU(cudaEventRecord(s->ev_grad[l], st));
     CU(cudaStreamWaitEvent(cs, s->ev_grad[l], 0));
     const int t = tbegin(s, 2, cs);
+    const Round16 own_code = round16_of(s, l, 1);  // the owner's coding of the mean (a8)
     switch (s->opt.exchange) {
-      case DFLOW_EXCHANGE_TRUNC16: {
+      case DFLOW_EXCHANGE_TRUNC16:
+      case DFLOW_EXCHANGE_SR16: {
         if (s->p2p) {
           // fused NVLink path: contributions already sit in our receive slots (pushed by the
           // peers' dW epilogues); fold, push q_bar to every rank, wait for every owner
-          ST(check_launch(s, launch_owner_reduce_p2p(ly.p2p, s->epoch, cs), 1, "owner reduce (p2p)"));
+          ST(check_launch(s, launch_owner_reduce_p2p(ly.p2p, s->epoch, cs, own_code), 1, "owner reduce (p2p)"));
           ST(check_launch(s, launch_wait_flags(ly.p2p.flags[s->opt.rank] + kMaxRanks, N, s->epoch, cs), 1,
                           "gather wait (p2p)"));
           g16 = ly.p2p.gath[s->opt.rank];
@@ -631,7 +650,9 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
         }
         NC(ncclAlltoAll(ly.q16, ly.recv, ly.shard * 2, ncclUint8, s->nccl, cs));
         ST(check_launch(s, launch_owner_reduce_t16(static_cast<uint16_t*>(ly.recv), ly.shard, N,
-                                                   static_cast<uint16_t*>(ly.own), cs), 1, "owner reduce"));
+                                                   static_cast<uint16_t*>(ly.own), cs, own_code,
+                                                   static_cast<int64_t>(s->opt.rank) * ly.shard),
+                        1, "owner reduce"));
         NC(ncclAllGather(ly.own, ly.gath, ly.shard * 2, ncclUint8, s->nccl, cs));
         g16 = static_cast<const uint16_t*>(ly.gath);
         g32 = nullptr;
@@ -674,20 +695,24 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
 
 // mode 0: train (TRUNC16 buckets + exchange + apply); 1: fetch (fp32 grads, no exchange)
 dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int mode) {
-  const bool t16 = mode == 0 && s->opt.world > 1 && s->opt.exchange == DFLOW_EXCHANGE_TRUNC16;
+  const bool t16 = mode == 0 && s->opt.world > 1 && u16_wire(s);
   for (int l = s->L - 1; l >= 0; --l) {
     Layer& ly = s->layers[l];
     if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
     const bool p2p = t16 && s->p2p;
-    ST(launch_gemm(s, p2p ? ly.wgrad_p2p
-                          : t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32),
-                   st));
+    const Round16 send_code = round16_of(s, l, 0);  // this rank's coding of its gradient (a6)
+    GemmPlan& wp = p2p ? ly.wgrad_p2p
+                       : t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32);
+    wp.args.r16 = send_code;
+    ST(launch_gemm(s, wp, st));
     // db_l: the producing epilogue left per-32-row column partials; sum them in order
     const int t = tbegin(s, 1, st);
     const int chunks = static_cast<int>((rows + 31) / 32);
-    cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, st)
+    cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, st,
+                                                  send_code)
                         : launch_colsum_final(ly.colsum_ws, chunks, ly.out, t16 ? nullptr : ly.g32 + ly.in * ly.out,
-                                              t16 ? ly.q16 + ly.in * ly.out : nullptr, st);
+                                              t16 ? ly.q16 + ly.in * ly.out : nullptr, st, send_code,
+                                              ly.in * ly.out);
     tend(s, t, st);
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
     if (mode == 0) ST(exchange_apply(s, l, st));
@@ -760,7 +785,7 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     return fail(DFLOW_INVALID_ARGUMENT, "need 0 <= rank < world");
   if (opt.precision != DFLOW_PRECISION_BF16 && opt.precision != DFLOW_PRECISION_3XTF32)
     return fail(DFLOW_INVALID_ARGUMENT, "unknown precision");
-  if (opt.exchange < DFLOW_EXCHANGE_TRUNC16 || opt.exchange > DFLOW_EXCHANGE_NONE)
+  if (opt.exchange < DFLOW_EXCHANGE_TRUNC16 || opt.exchange > DFLOW_EXCHANGE_SR16)
     return fail(DFLOW_INVALID_ARGUMENT, "unknown exchange mode");
   if (opt.max_local_rows <= 0) return fail(DFLOW_INVALID_ARGUMENT, "max_local_rows must be > 0");
   if (opt.world > 1 && !nccl_id) return fail(DFLOW_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
@@ -769,7 +794,8 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   s->cap = opt.max_local_rows;
   s->tf32 = opt.precision == DFLOW_PRECISION_3XTF32;
   s->esz = s->tf32 ? 4 : 2;
-  s->p2p = opt.p2p && opt.world > 1 && opt.exchange == DFLOW_EXCHANGE_TRUNC16;
+  s->p2p = opt.p2p && opt.world > 1 &&
+           (opt.exchange == DFLOW_EXCHANGE_TRUNC16 || opt.exchange == DFLOW_EXCHANGE_SR16);
   dflow_status st = insert_exchange(user, opt.world, opt.exchange, &s->g, &s->remap);
   if (st == DFLOW_OK) st = match_graph(s);
   if (st == DFLOW_OK && s->tf32 && s->x_dtype != DFLOW_F32)
@@ -1059,7 +1085,14 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
     return DFLOW_OK;
   }
   const int64_t npad = pad_to(static_cast<int64_t>(n), 8 * N), shard = npad / N;
-  const size_t esz = s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 ? 2 : 4;
+  const bool w16 = u16_wire(s);
+  const size_t esz = w16 ? 2 : 4;
+  // SR16 draws of standalone exchange i (1-based): step i, layer 0 (reading A27)
+  const uint32_t xstep = ++s->xchg_calls;
+  const bool sr = s->opt.exchange == DFLOW_EXCHANGE_SR16;
+  const uint32_t R = static_cast<uint32_t>(s->opt.rank);
+  const Round16 send_code{sr ? round16_key(s->opt.sr_seed, xstep, 0, 0, R) : 0u, sr ? 1 : 0};
+  const Round16 own_code{sr ? round16_key(s->opt.sr_seed, xstep, 0, 1, R) : 0u, sr ? 1 : 0};
   if (s->xbuf_bytes < static_cast<size_t>(npad) * 4) {  // grow-only scratch (send, recv, own, gath)
     CU(cudaStreamSynchronize(st));
     CU(cudaStreamSynchronize(s->comm));
@@ -1074,8 +1107,8 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
   void *send = s->xbuf[0], *recv = s->xbuf[1], *own = s->xbuf[2], *gath = s->xbuf[3];
   CU(cudaMemsetAsync(send, 0, npad * esz, st));
   cudaError_t e = cudaSuccess;
-  if (s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
-    e = launch_truncate16(grad, static_cast<uint16_t*>(send), n, st);
+  if (w16) {
+    e = launch_round16(grad, static_cast<uint16_t*>(send), n, send_code, 0, st);
   } else {
     e = cudaMemcpyAsync(send, grad, n * sizeof(float), cudaMemcpyDeviceToDevice, st);
   }
@@ -1083,9 +1116,10 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
   CU(cudaEventRecord(s->ev_loss, st));
   CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
   cudaStream_t cs = s->comm;
-  if (s->opt.exchange == DFLOW_EXCHANGE_TRUNC16) {
+  if (w16) {
     NC(ncclAlltoAll(send, recv, shard * 2, ncclUint8, s->nccl, cs));
-    CU(launch_owner_reduce_t16(static_cast<uint16_t*>(recv), shard, N, static_cast<uint16_t*>(own), cs));
+    CU(launch_owner_reduce_t16(static_cast<uint16_t*>(recv), shard, N, static_cast<uint16_t*>(own), cs, own_code,
+                               static_cast<int64_t>(s->opt.rank) * shard));
     NC(ncclAllGather(own, gath, shard * 2, ncclUint8, s->nccl, cs));
     CU(launch_expand16(static_cast<uint16_t*>(gath), out, n, cs));
   } else if (s->opt.exchange == DFLOW_EXCHANGE_FP32) {

@@ -85,6 +85,7 @@ struct dflow_session {
   int64_t mask_words_cap = 0;
   void* xbuf[4] = {nullptr, nullptr, nullptr, nullptr};  // dflow_exchange scratch (grow-only)
   size_t xbuf_bytes = 0;
+  uint32_t xchg_calls = 0;  // standalone dflow_exchange calls (the SR16 step counter there)
   void* host_stage[2] = {nullptr, nullptr};  // device copies of host feeds (e2e path)
   size_t host_stage_bytes[2] = {0, 0};
   cudaStream_t comm = nullptr;

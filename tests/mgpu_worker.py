@@ -31,8 +31,9 @@ import synth  # noqa: E402
 
 def main(out_path, exchange):
     p2p = 0
-    if exchange == "TRUNC16_P2P":  # the fused NVLink exchange (f1): same bits as the NCCL path
-        exchange, p2p = "TRUNC16", 1
+    if exchange.endswith("_P2P"):  # the fused NVLink exchange (f1): same bits as the NCCL path
+        exchange, p2p = exchange[:-4], 1
+    seed = 1234  # SR16 draw streams (reading A27)
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -50,7 +51,7 @@ def main(out_path, exchange):
     X, Y = synth.batch(w)
     Xr, Yr = X[rank * b:(rank + 1) * b], Y[rank * b:(rank + 1) * b]
     run = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local, nccl_id=nid,
-              p2p=p2p)
+              p2p=p2p, sr_seed=seed)
     run.assign(Ws, bs)
     Xd, Yd = torch.from_numpy(Xr).cuda(), torch.from_numpy(Yr).cuda()
 
@@ -62,7 +63,8 @@ def main(out_path, exchange):
     D.check(D.dflow_exchange(run.s, C.c_void_p(gd.data_ptr()), C.c_void_p(outd.data_ptr()), n, stream_ptr()))
     torch.cuda.synchronize()
     all_g = [synth.rng(500 + r).standard_normal(n).astype(np.float32) for r in range(world)]
-    ref = combine(all_g, exchange if exchange != "FP32_NCCL" else "FP32")
+    # (the first standalone exchange of the session: SR16 step 1, layer 0)
+    ref = combine(all_g, exchange if exchange != "FP32_NCCL" else "FP32", sr=(seed, 1, 0))
     got = outd.cpu().numpy()
     if exchange == "FP32_NCCL":
         verdict["p4_exchange_max_rel"] = normwise(got, ref)
@@ -88,6 +90,19 @@ def main(out_path, exchange):
     verdict["p11_replicas_identical"] = all(bool(torch.equal(allW[0], x)) for x in allW)
 
     # P4': oracle exchange + apply of the GPU's own gradients == the GPU step, bit for bit
+    if exchange == "SR16":
+        # per layer bucket [dW_l ; db_l], the session's first train step (epoch 1)
+        ok = True
+        off = 0
+        for l in range(w.layers):
+            nw, nb = Ws[l].size, bs[l].size
+            ghat = combine([p[off:off + nw + nb] for p in per_rank], "SR16", sr=(seed, 1, l))
+            new_w = OK.apply_gradient_descent(Ws[l], w.lr, ghat[:nw].reshape(Ws[l].shape), "f32")
+            new_b = OK.apply_gradient_descent(bs[l], w.lr, ghat[nw:], "f32")
+            ok &= bool(np.array_equal(new_w.view(np.uint32), Wg[l].view(np.uint32)))
+            ok &= bool(np.array_equal(new_b.view(np.uint32), bg[l].view(np.uint32)))
+            off += nw + nb
+        verdict["p4_step_bitexact"] = ok
     if exchange in ("TRUNC16", "FP32"):
         ok = True
         off = 0
@@ -103,7 +118,7 @@ def main(out_path, exchange):
 
     # gate: vs the oracle's N-replica step on the same global batch
     mg = build_mlp(w.dims, "MSE", w.lr)
-    ref = train_step(mg, Ws, bs, X, Y, world, exchange if exchange != "FP32_NCCL" else "FP32")
+    ref = train_step(mg, Ws, bs, X, Y, world, exchange if exchange != "FP32_NCCL" else "FP32", sr_seed=seed, step=1)
     errs = [normwise(a, r) for a, r in zip(Wg + bg, ref["W"] + ref["b"])]
     verdict["w_after_max_err"] = max(errs)
     verdict["loss_rel_err"] = abs(loss - ref["loss"]) / ref["loss"]

@@ -83,7 +83,8 @@ def _session_graph_json_or_status(m, world, exchange):
     return D.dflow_session_create(m.graph, C.byref(opts), fake_id, C.byref(s)), s
 
 
-@pytest.mark.parametrize("world,exchange", [(1, "TRUNC16"), (2, "TRUNC16"), (4, "FP32"), (2, "FP32_NCCL")])
+@pytest.mark.parametrize("world,exchange", [(1, "TRUNC16"), (2, "TRUNC16"), (4, "FP32"), (2, "FP32_NCCL"),
+                                            (2, "SR16")])
 def test_planner_accepts_mlp_graphs(world, exchange):
     m = D.mlp_graph((16, 8, 4), "MSE", 0.5)
     st, s = _session_graph_json_or_status(m, world, exchange)
@@ -124,7 +125,7 @@ def test_planner_rejects_graph_without_relu_grad():
 
 
 @pytest.mark.parametrize("world,exchange", [(1, "TRUNC16"), (2, "TRUNC16"), (4, "TRUNC16"), (2, "FP32"),
-                                            (8, "FP32_NCCL"), (2, "NONE")])
+                                            (8, "FP32_NCCL"), (2, "NONE"), (4, "SR16"), (1, "SR16")])
 def test_compression_pass_matches_oracle_pass(world, exchange):
     # The C pass (insert_exchange) and the oracle's produce the same rewritten graph.
     dims = (16, 8, 4)
@@ -136,12 +137,26 @@ def test_compression_pass_matches_oracle_pass(world, exchange):
         ref = OG.insert_exchange(mg.graph, world, exchange)
         assert _canon(D.graph_json(out)) == _canon(ref.to_json())
         names = [n.name for n in ref.nodes]
-        if world > 1 and exchange == "TRUNC16":
+        if world > 1 and exchange in ("TRUNC16", "SR16"):
+            code = "trunc16" if exchange == "TRUNC16" else "sround16"
             for v in ("W1", "b1", "W2", "b2"):
                 i = names.index(f"update/{v}")
-                assert names[i - 3:i] == [f"xchg/{v}/trunc16", f"xchg/{v}/mean", f"xchg/{v}/expand16"]
+                assert names[i - 3:i] == [f"xchg/{v}/{code}", f"xchg/{v}/mean", f"xchg/{v}/expand16"]
         if world == 1 or exchange == "NONE":
             assert ref.to_json() == mg.graph.to_json()
     finally:
         D.dflow_graph_destroy(out)
         D.dflow_graph_destroy(m.graph)
+
+
+def test_round16_key_matches_the_oracle_key_derivation():
+    # host code of the product vs the oracle's independent implementation (reading A27)
+    from oracle.codec import sr_key
+    k = C.c_uint32()
+    for seed in (0, 1, 0xDEADBEEF):
+        for step in (1, 2, 77):
+            for layer in (0, 3):
+                for stage in (0, 1):
+                    for rank in (0, 5):
+                        D.check(D.dflow_round16_key(seed, step, layer, stage, rank, C.byref(k)))
+                        assert k.value == sr_key(seed, step, layer, stage, rank)

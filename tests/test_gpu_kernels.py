@@ -12,7 +12,8 @@ pytestmark = pytest.mark.gpu
 
 import paper_1603_04467_b200 as D  # noqa: E402
 from oracle import kernels as OK  # noqa: E402
-from oracle.codec import expand16, truncate16  # noqa: E402
+from oracle.codec import expand16, sr16, sr_key, sr_random, truncate16  # noqa: E402
+from synth import random_f32_bits  # noqa: E402
 from synth import rng  # noqa: E402
 from dflow_harness import stream_ptr  # noqa: E402
 
@@ -56,6 +57,22 @@ def test_codec_ragged_lengths(n):
     D.check(D.dflow_truncate16(_vp(src), _vp(q), n, stream_ptr()))
     if n:
         assert np.array_equal(q.cpu().numpy()[:n].view(np.uint16), truncate16(x))
+
+
+@pytest.mark.parametrize("n,idx_base", [(1, 0), (9, 0), (4099, 0), (1 << 20, 0), (1000, 123456789)])
+def test_sr16_kernel_bit_exact_vs_oracle(n, idx_base):
+    # f2: the SR16 coding (readings A26-A27) on random bit patterns (incl. specials): GPU
+    # codes == the oracle's (bits + r) >> 16 with its own generator's draws
+    x = random_f32_bits(n)
+    key = sr_key(77, 3, 2, 0, 1)
+    src = torch.from_numpy(x.view(np.int32)).cuda()
+    q = torch.empty(n, dtype=torch.int16, device="cuda")
+    D.check(D.dflow_round16(_vp(src), _vp(q), n, key, 1, idx_base, stream_ptr()))
+    exp = sr16(x, sr_random(key, np.arange(idx_base, idx_base + n)))
+    assert np.array_equal(q.cpu().numpy().view(np.uint16), exp)
+    # stochastic = 0 is plain truncation
+    D.check(D.dflow_round16(_vp(src), _vp(q), n, key, 0, idx_base, stream_ptr()))
+    assert np.array_equal(q.cpu().numpy().view(np.uint16), truncate16(x))
 
 
 # ---------------------------------------------------------------- GEMM

@@ -31,7 +31,7 @@ def _run(n, exchange, tmp_path):
     return json.load(open(out))
 
 
-@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL"])
+@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL", "SR16", "SR16_P2P"])
 def test_two_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 2:
@@ -45,7 +45,7 @@ def test_two_gpu_replicated_step(exchange, tmp_path):
     assert v["w_after_max_err"] < 2e-2, v
 
 
-@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P"])
+@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "SR16_P2P"])
 def test_four_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 4:
