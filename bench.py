@@ -222,6 +222,7 @@ def run_gpu(args, w):
     mlp = D.mlp_graph(w.dims, w.loss, w.lr)
     opts = D.make_options(world=world, rank=rank, device=local, exchange=args.exchange, max_local_rows=b,
                           overlap=1, sm_reserve=args.sm_reserve, p2p=args.p2p, sr_seed=1234,
+                          graphs=1 if world == 1 else 0,
                           precision=D.DFLOW_PRECISION_3XTF32 if tf32 else D.DFLOW_PRECISION_BF16)
     s = D.session_create(mlp, opts, nid)
     Ws, bs = synth.init_params(w)

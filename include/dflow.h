@@ -139,6 +139,10 @@ typedef struct {
                              truncated tiles into the owners' buffers through CUDA IPC peer
                              pointers; owner fold + all-gather by peer stores); 0 = NCCL calls  */
   uint32_t sr_seed;       /* SR16: seed of the counter-based draw streams (reading A27)        */
+  int32_t graphs;         /* world == 1: 1 = capture the train step into a CUDA graph per feed
+                             signature (x, y pointers, leading dims, rows) and replay it — one
+                             launch per step instead of ~4L host launches (latency-bound C2);
+                             the captured kernels and their arguments are the same             */
 } dflow_options;
 
 /* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */

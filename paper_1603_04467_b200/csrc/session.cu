@@ -331,6 +331,10 @@ dflow_status alloc_state(dflow_session* s) {
   cudaEventCreateWithFlags(&s->ev_loss_ready, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&s->ev_h2d_y, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_gin, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_gout, cudaEventDisableTiming);
+  if (cudaStreamCreateWithFlags(&s->gstream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(DFLOW_CUDA, "stream creation failed");
   cudaEventCreateWithFlags(&s->ev_feeds_free, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking) != cudaSuccess)
     return fail(DFLOW_CUDA, "stream creation failed");
@@ -606,7 +610,8 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
     p.args.y = f.y;
     p.args.ldy = f.ldy;
     if (s->y_upload_pending) {  // host-fed y still uploading under layers 1..L-1
-      CU(cudaStreamWaitEvent(st, s->ev_h2d_y, 0));
+      // (inside a step-graph capture this becomes an external event-wait node)
+      CU(cudaStreamWaitEvent(st, s->ev_h2d_y, s->capturing ? cudaEventWaitExternal : 0));
       s->y_upload_pending = false;
     }
     ST(launch_gemm(s, p, st));
@@ -740,6 +745,11 @@ dflow_status finish_timing(dflow_session* s, cudaStream_t st) {
 // The loss is final when the forward ends (k_loss_final): its device->host copy is
 // enqueued right after the forward and waited for after the backward has been enqueued,
 // so the host returns while the backward and the update still run (stream-ordered).
+// Event record that may sit inside a step-graph capture (and is waited on outside it).
+cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st) {
+  return s->capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+}
+
 dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
   if (s->opt.world > 1) {
     CU(cudaEventRecord(s->ev_loss, st));
@@ -749,7 +759,7 @@ dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
     CU(cudaEventRecord(s->ev_loss_ready, s->comm));
   } else {
     CU(cudaMemcpyAsync(s->loss_host, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
-    CU(cudaEventRecord(s->ev_loss_ready, st));
+    CU(record_event(s, s->ev_loss_ready, st));
   }
   s->loss_pending = true;
   return DFLOW_OK;
@@ -863,8 +873,10 @@ void session_destroy(dflow_session* s) {
   for (cudaEvent_t e : s->ev_apply) cudaEventDestroy(e);
   for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
   if (s->ev_loss) cudaEventDestroy(s->ev_loss);
-  for (cudaEvent_t e : {s->ev_loss_ready, s->ev_h2d, s->ev_h2d_y, s->ev_feeds_free})
+  for (auto& g : s->step_graphs) cudaGraphExecDestroy(g.exec);
+  for (cudaEvent_t e : {s->ev_loss_ready, s->ev_h2d, s->ev_h2d_y, s->ev_feeds_free, s->ev_gin, s->ev_gout})
     if (e) cudaEventDestroy(e);
+  if (s->gstream) cudaStreamDestroy(s->gstream);
   if (s->h2d) cudaStreamDestroy(s->h2d);
   if (s->comm) cudaStreamDestroy(s->comm);
   cudaGetLastError();
@@ -877,15 +889,60 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   ST(check_rows(s, rows));
   Feeds f;
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
-  s->launches = s->gemm_launches = 0;
-  s->epoch++;  // p2p exchange flags of this step
-  ST(run_forward(s, f, rows, st, FWD_TRAIN));
-  CU(cudaEventRecord(s->ev_feeds_free, st));  // x and y are not read after the forward
-  if (loss_out) ST(enqueue_loss(s, st));
-  ST(run_backward(s, rows, st, 0));
+  s->epoch++;  // p2p exchange flags / SR16 draws of this step
+  // one step's work on `stream` (also what a step graph captures)
+  auto body = [&](cudaStream_t stream) -> dflow_status {
+    s->launches = s->gemm_launches = 0;
+    ST(run_forward(s, f, rows, stream, FWD_TRAIN));
+    CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
+    if (loss_out) ST(enqueue_loss(s, stream));
+    ST(run_backward(s, rows, stream, 0));
+    s->last_launches = s->launches;
+    s->last_gemm_launches = s->gemm_launches;
+    return DFLOW_OK;
+  };
+  if (s->opt.graphs && s->opt.world == 1 && !s->timing) {
+    dflow_session::StepGraph* g = nullptr;
+    const bool ywait = s->y_upload_pending;  // host-fed y: the graph holds an external wait before the last GEMM
+    for (auto& e : s->step_graphs)
+      if (e.x == f.x && e.y == f.y && e.ldx == f.ldx && e.ldy == f.ldy && e.rows == rows &&
+          e.loss == (loss_out != nullptr) && e.ywait == ywait)
+        g = &e;
+    s->y_upload_pending = false;
+    if (!g) {
+      s->y_upload_pending = ywait;
+      CU(cudaStreamBeginCapture(s->gstream, cudaStreamCaptureModeThreadLocal));
+      s->capturing = true;
+      const dflow_status r = body(s->gstream);
+      s->capturing = false;
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(s->gstream, &graph);
+      if (r != DFLOW_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return r;
+      }
+      CU(ec);
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      CU(ei);
+      if (s->step_graphs.size() >= 8) {  // bounded cache: drop the oldest
+        cudaGraphExecDestroy(s->step_graphs.front().exec);
+        s->step_graphs.erase(s->step_graphs.begin());
+      }
+      s->step_graphs.push_back({f.x, f.y, f.ldx, f.ldy, rows, loss_out != nullptr, ywait, exec});
+      g = &s->step_graphs.back();
+    }
+    CU(cudaEventRecord(s->ev_gin, st));
+    CU(cudaStreamWaitEvent(s->gstream, s->ev_gin, 0));
+    CU(cudaGraphLaunch(g->exec, s->gstream));
+    CU(cudaEventRecord(s->ev_gout, s->gstream));
+    CU(cudaStreamWaitEvent(st, s->ev_gout, 0));
+    if (loss_out) s->loss_pending = true;
+  } else {
+    ST(body(st));
+  }
   CU(cudaGetLastError());
-  s->last_launches = s->launches;
-  s->last_gemm_launches = s->gemm_launches;
   ST(wait_loss(s, loss_out));
   if (s->timing) {
     ST(finish_timing(s, st));

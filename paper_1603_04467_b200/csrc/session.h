@@ -100,6 +100,19 @@ struct dflow_session {
   cudaStream_t h2d = nullptr;
   cudaEvent_t ev_h2d = nullptr, ev_h2d_y = nullptr, ev_feeds_free = nullptr;
   bool y_upload_pending = false;
+  // opt.graphs: captured train steps keyed by their feed signature, replayed on gstream
+  struct StepGraph {
+    const void* x;
+    const void* y;
+    int64_t ldx, ldy, rows;
+    bool loss;
+    bool ywait;
+    cudaGraphExec_t exec;
+  };
+  std::vector<StepGraph> step_graphs;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t ev_gin = nullptr, ev_gout = nullptr;
+  bool capturing = false;
   ncclComm_t nccl = nullptr;
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;

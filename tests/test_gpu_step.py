@@ -199,3 +199,62 @@ def test_host_fed_steps_match_device_fed_bitwise():
     finally:
         dev.close()
         host.close()
+
+
+def test_p15_non_finite_guard():
+    # PAPER.md:879 (lesson 5, non-finite checks): a NaN / Inf reaching the step shows up in
+    # the loss and the session's nonfinite flag; a clean step clears it
+    w = with_batch(C2, 64)
+    Ws, bs = init_params(w)
+    run = Run(w.dims, "MSE", w.lr, rows=w.batch)
+    try:
+        run.assign(Ws, bs)
+        X, Y = batch(w)
+        assert np.isfinite(run.step(_dev(X), _dev(Y))) and run.stats().nonfinite == 0
+        for bad in (np.nan, np.inf):
+            Yb = Y.copy()
+            Yb[3, 5] = bad
+            loss = run.step(_dev(X), _dev(Yb))
+            assert not np.isfinite(loss) and run.stats().nonfinite == 1
+            run.assign(Ws, bs)  # the poisoned update is discarded by re-assigning
+        assert np.isfinite(run.step(_dev(X), _dev(Y))) and run.stats().nonfinite == 0
+    finally:
+        run.close()
+
+
+def test_step_graphs_replay_bitwise():
+    # opt.graphs: the captured-and-replayed step computes exactly what the launched one does,
+    # for device feeds (two feed signatures -> two graphs) and host feeds
+    w = with_batch(C2, 256)
+    Ws, bs = init_params(w)
+    plain = Run(w.dims, "MSE", w.lr, rows=w.batch)
+    graph = Run(w.dims, "MSE", w.lr, rows=w.batch, graphs=1)
+    try:
+        plain.assign(Ws, bs)
+        graph.assign(Ws, bs)
+        bufs = [(_dev(batch(w, step=k)[0]), _dev(batch(w, step=k)[1])) for k in range(2)]
+        for step in range(6):
+            X, Y = batch(w, step=step)
+            Xd, Yd = bufs[step % 2]
+            Xd.copy_(torch.from_numpy(X))
+            Yd.copy_(torch.from_numpy(Y))
+            lp = plain.step(Xd, Yd)
+            lg = graph.step(Xd, Yd, want_loss=(step != 3))
+            if step != 3:
+                assert np.float32(lp).view(np.uint32) == np.float32(lg).view(np.uint32), step
+        ids, lds = D.node_array([graph.mlp.x, graph.mlp.y]), D.i64_array([w.dims[0], w.dims[-1]])
+        for step in range(6, 9):
+            X, Y = batch(w, step=step)
+            lp = plain.step(_dev(X), _dev(Y))
+            Xh, Yh = torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory()
+            lh = C.c_float(0)
+            D.check(D.dflow_train_step_host(graph.s, 2, ids, D.ptr_array([Xh.data_ptr(), Yh.data_ptr()]), lds,
+                                            w.batch, C.byref(lh), stream_ptr()))
+            assert np.float32(lp).view(np.uint32) == np.float32(lh.value).view(np.uint32), step
+        Wp, bp = plain.read()
+        Wg, bg = graph.read()
+        for a, b in zip(Wp + bp, Wg + bg):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    finally:
+        plain.close()
+        graph.close()
