@@ -309,7 +309,7 @@ def run_gpu(args, w):
     achieved = mma_mult * flops_per_launch / (gemm_avg_ms / 1000.0) / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1 and not args.batch:  # profiled at N = 1, the full batch
         try:
             traffic = json.load(open(tp)).get(w.name)
         except Exception:
