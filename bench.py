@@ -189,8 +189,9 @@ def run_reference(args, w):
 def config_dict(w, args, world):
     return {"workload": w.name, "global_batch": w.batch, "layers": w.layers, "width": w.dims[1],
             "dims": list(w.dims), "loss": w.loss, "lr": w.lr,
-            "exchange": args.exchange + ("_P2P" if (args.exchange in ("TRUNC16", "SR16") and world > 1 and
-                                                   getattr(args, "p2p", 0)) else ""),
+            "exchange": ("ASYNC_" if (world > 1 and getattr(args, "async_dp", 0)) else "") + args.exchange +
+                        ("_P2P" if (args.exchange in ("TRUNC16", "SR16") and world > 1 and getattr(args, "p2p", 0)
+                                    and not getattr(args, "async_dp", 0)) else ""),
             "parallelism": f"dp{world}",
             "precision": ("3xTF32 split fp32 operands (big, small), fp32 accumulate + master weights"
                           if w.precision == "3xtf32" else "bf16 operands, fp32 accumulate + master weights"),
@@ -222,7 +223,7 @@ def run_gpu(args, w):
     mlp = D.mlp_graph(w.dims, w.loss, w.lr)
     opts = D.make_options(world=world, rank=rank, device=local, exchange=args.exchange, max_local_rows=b,
                           overlap=1, sm_reserve=args.sm_reserve, p2p=args.p2p, sr_seed=1234,
-                          graphs=1 if world == 1 else 0,
+                          graphs=1 if world == 1 else 0, async_dp=args.async_dp if world > 1 else 0,
                           precision=D.DFLOW_PRECISION_3XTF32 if tf32 else D.DFLOW_PRECISION_BF16)
     s = D.session_create(mlp, opts, nid)
     Ws, bs = synth.init_params(w)
@@ -367,6 +368,9 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="override the global batch (parity/debug only)")
     ap.add_argument("--exchange", default="TRUNC16", choices=["TRUNC16", "FP32", "FP32_NCCL", "NONE", "SR16"])
+    ap.add_argument("--async-dp", type=int, default=0,
+                    help="N > 1: 1 = asynchronous replicas (f3): each rank pulls the shared parameters, steps "
+                         "and pushes its own coded update with no barrier (the exchange names the coding)")
     ap.add_argument("--sm-reserve", type=int, default=0)
     ap.add_argument("--p2p", type=int, default=1,
                     help="TRUNC16 at N > 1: 1 = fused NVLink exchange (dW epilogue stores into the owners' "

@@ -122,6 +122,8 @@ dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int ex
 #define DFLOW_EXCHANGE_FP32 1     /* same schedule with fp32 payloads (deterministic)              */
 #define DFLOW_EXCHANGE_FP32_NCCL 2 /* ncclAllReduce(sum, fp32) then x 1/N (library baseline)        */
 #define DFLOW_EXCHANGE_NONE 3     /* debug/timing only: no exchange (N>1 results are wrong)        */
+#define DFLOW_EXCHANGE_ASYNC 0x100 /* flag for dflow_graph_insert_exchange: the asynchronous-replica
+                                      channel (f3): code -> expand -> apply, no cross-replica mean */
 #define DFLOW_EXCHANGE_SR16 4     /* TRUNC16's schedule with both 32->16 codings done by stochastic
                                      rounding (f2; "probabilistic rounding";
                                      readings A26-A28; draws keyed by options.sr_seed)           */
@@ -139,6 +141,13 @@ typedef struct {
                              truncated tiles into the owners' buffers through CUDA IPC peer
                              pointers; owner fold + all-gather by peer stores); 0 = NCCL calls  */
   uint32_t sr_seed;       /* SR16: seed of the counter-based draw streams (reading A27)        */
+  int32_t async_dp;       /* world > 1, bf16: 1 = asynchronous replicas (f3):
+                             each train step pulls the shared (sharded) parameters over NVLink,
+                             computes its gradient and pushes -lr * g_hat into the owners'
+                             shards with NVLink reductions — no mean, no barrier (readings
+                             A29-A31; exchange TRUNC16 / SR16 / FP32 = the coding of the
+                             cross-device pushes); 2 = the same without the automatic pull
+                             (the client calls dflow_async_pull)                             */
   int32_t graphs;         /* world == 1: 1 = capture the train step into a CUDA graph per feed
                              signature (x, y pointers, leading dims, rows) and replay it — one
                              launch per step instead of ~4L host launches (latency-bound C2);
@@ -180,6 +189,10 @@ dflow_status dflow_train_step(dflow_session* s, int n_feeds, const dflow_node* f
 dflow_status dflow_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                    const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
                                    float* loss_out, void* stream);
+/* async_dp sessions: this replica's local parameters (and operand copies) <- the current
+ * shared shards of every rank (NVLink loads), stream-ordered on `stream`.  The updates
+ * other replicas push concurrently may or may not be included (no lock, reading A29). */
+dflow_status dflow_async_pull(dflow_session* s, void* stream);
 /* Fig.1 "s.run(C, feed_dict={x: input})": forward only, no update.  fetch is a
  * Relu node (writes fp32 [local_rows, out] dense) or the cost (writes 1 fp32). */
 dflow_status dflow_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* dev_ptrs,

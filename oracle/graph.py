@@ -273,28 +273,29 @@ class Graph:
         return json.dumps({"version": 1, "nodes": [n.to_dict() for n in self.nodes]}, sort_keys=True)
 
 
-def insert_exchange(graph: Graph, world: int, exchange: str) -> Graph:
+def insert_exchange(graph: Graph, world: int, exchange: str, asynchronous: bool = False) -> Graph:
     """Compression-insertion on the replica->combine transfer (PAPER.md :813-821 on the
     §7 :934-941 channel; SPEC.md:681-689 shape).  For world > 1, between every
     ApplyGradientDescent and its gradient: TRUNC16 -> Truncate16, CrossReplicaMeanT16
     (attr world), Expand16; SR16 -> StochasticRound16, CrossReplicaMeanSR16, Expand16;
-    FP32 modes -> CrossReplicaMean.  world == 1 or NONE: a copy
+    FP32 modes -> CrossReplicaMean.  asynchronous (f3): every replica
+    applies its own coded gradient — the code and Expand16 nodes without the mean; FP32:
+    nothing (no coding, no mean).  world == 1 or NONE: a copy
     (reading A6).  The replicas themselves are implicit (one per rank)."""
     out = Graph()
-    active = world > 1 and exchange != "NONE"
+    active = world > 1 and exchange != "NONE" and not (asynchronous and exchange.startswith("FP32"))
     for n in graph.nodes:
         inputs = list(n.inputs)
         if active and n.op == "ApplyGradientDescent":
             var, g = inputs
             G = out.by_name[g]
-            if exchange == "TRUNC16":
-                t = out._add(f"xchg/{var}/trunc16", "Truncate16", [g], {}, "u16", G.shape)
-                m = out._add(f"xchg/{var}/mean", "CrossReplicaMeanT16", [t], {"world": world}, "u16", G.shape)
-                inputs[1] = out._add(f"xchg/{var}/expand16", "Expand16", [m], {}, "f32", G.shape)
-            elif exchange == "SR16":
-                t = out._add(f"xchg/{var}/sround16", "StochasticRound16", [g], {}, "u16", G.shape)
-                m = out._add(f"xchg/{var}/mean", "CrossReplicaMeanSR16", [t], {"world": world}, "u16", G.shape)
-                inputs[1] = out._add(f"xchg/{var}/expand16", "Expand16", [m], {}, "f32", G.shape)
+            if exchange in ("TRUNC16", "SR16"):
+                code, mean = (("trunc16", "Truncate16"), "CrossReplicaMeanT16") if exchange == "TRUNC16" else \
+                    (("sround16", "StochasticRound16"), "CrossReplicaMeanSR16")
+                t = out._add(f"xchg/{var}/{code[0]}", code[1], [g], {}, "u16", G.shape)
+                if not asynchronous:
+                    t = out._add(f"xchg/{var}/mean", mean, [t], {"world": world}, "u16", G.shape)
+                inputs[1] = out._add(f"xchg/{var}/expand16", "Expand16", [t], {}, "f32", G.shape)
             else:
                 inputs[1] = out._add(f"xchg/{var}/mean", "CrossReplicaMean", [g], {"world": world}, "f32", G.shape)
         out._add(n.name, n.op, inputs, n.attrs, n.dtype, n.shape)

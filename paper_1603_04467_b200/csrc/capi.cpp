@@ -184,7 +184,8 @@ dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, si
 dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int exchange, dflow_graph** out) {
   GUARD_BEGIN
   if (!g || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
-  if (world < 1 || exchange < DFLOW_EXCHANGE_TRUNC16 || exchange > DFLOW_EXCHANGE_SR16)
+  const int ex = exchange & ~DFLOW_EXCHANGE_ASYNC;
+  if (world < 1 || ex < DFLOW_EXCHANGE_TRUNC16 || ex > DFLOW_EXCHANGE_SR16 || (exchange & ~0x1FF))
     return fail(DFLOW_INVALID_ARGUMENT, "bad world/exchange");
   dflow_graph* r = new dflow_graph();
   std::vector<int> remap;
@@ -334,6 +335,13 @@ dflow_status dflow_expand16(const uint16_t* src, float* dst, size_t n, void* str
   cudaError_t e = dflow::launch_expand16(src, dst, n, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(DFLOW_CUDA, "expand16: %s", cudaGetErrorString(e));
   return DFLOW_OK;
+}
+
+dflow_status dflow_async_pull(dflow_session* s, void* stream) {
+  GUARD_BEGIN
+  if (!s) return fail(DFLOW_INVALID_ARGUMENT, "session is NULL");
+  return dflow::session_async_pull(s, static_cast<cudaStream_t>(stream));
+  GUARD_END
 }
 
 dflow_status dflow_exchange(dflow_session* s, const float* grad_dev, float* out_dev, size_t n, void* stream) {

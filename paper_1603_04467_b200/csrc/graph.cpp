@@ -431,7 +431,11 @@ std::string Graph::to_json() const {
 dflow_status insert_exchange(const Graph& in, int world, int exchange, Graph* out, std::vector<int>* remap) {
   *out = Graph();
   remap->assign(in.nodes.size(), -1);
-  const bool active = world > 1 && exchange != DFLOW_EXCHANGE_NONE;
+  // asynchronous replicas (f3): each replica's coded gradient goes straight to the apply
+  const bool async = (exchange & DFLOW_EXCHANGE_ASYNC) != 0;
+  exchange &= ~DFLOW_EXCHANGE_ASYNC;
+  const bool active = world > 1 && exchange != DFLOW_EXCHANGE_NONE &&
+                      !(async && (exchange == DFLOW_EXCHANGE_FP32 || exchange == DFLOW_EXCHANGE_FP32_NCCL));
   for (size_t i = 0; i < in.nodes.size(); ++i) {
     Node n = in.nodes[i];
     for (int& k : n.inputs) k = (*remap)[k];
@@ -450,14 +454,16 @@ dflow_status insert_exchange(const Graph& in, int world, int exchange, Graph* ou
         t.dtype = DFLOW_U16;
         t.shape = gnode.shape;
         if ((st = out->append(t, &id))) return st;
-        Node m;
-        m.name = "xchg/" + var + "/mean";
-        m.op = sr ? Op::CrossReplicaMeanSR16 : Op::CrossReplicaMeanT16;
-        m.inputs = {id};
-        m.dtype = DFLOW_U16;
-        m.shape = gnode.shape;
-        m.world = world;
-        if ((st = out->append(m, &id))) return st;
+        if (!async) {
+          Node m;
+          m.name = "xchg/" + var + "/mean";
+          m.op = sr ? Op::CrossReplicaMeanSR16 : Op::CrossReplicaMeanT16;
+          m.inputs = {id};
+          m.dtype = DFLOW_U16;
+          m.shape = gnode.shape;
+          m.world = world;
+          if ((st = out->append(m, &id))) return st;
+        }
         Node e;
         e.name = "xchg/" + var + "/expand16";
         e.op = Op::Expand16;

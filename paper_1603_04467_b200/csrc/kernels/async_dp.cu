@@ -1,0 +1,92 @@
+// Asynchronous data-parallel pull / push kernels (f3).  See async_dp.h.
+#include <algorithm>
+
+#include "async_dp.h"
+
+namespace dflow {
+namespace {
+
+__device__ __forceinline__ float ld_relaxed_sys(const float* p) {
+  float v;
+  asm volatile("ld.relaxed.sys.global.f32 %0, [%1];" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+
+int grid_for(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8))); }
+
+__global__ void k_async_pull(const AsyncLayer a, float* __restrict__ W32, float* __restrict__ b32,
+                             __nv_bfloat16* __restrict__ wop, int64_t ldwb) {
+  const int64_t nw = a.in * a.out, p = nw + a.out;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p; i += stride) {
+    const int owner = static_cast<int>(i / a.shard);
+    const float v = ld_relaxed_sys(a.master[owner] + (i - static_cast<int64_t>(owner) * a.shard));
+    if (i < nw) {
+      W32[i] = v;
+      wop[(i / a.out) * ldwb + i % a.out] = __float2bfloat16_rn(v);  // operand copy (reading A13)
+    } else {
+      b32[i - nw] = v;
+    }
+  }
+}
+
+__global__ void k_async_publish(const AsyncLayer a, const float* __restrict__ W32, const float* __restrict__ b32) {
+  const int64_t nw = a.in * a.out, p = nw + a.out;
+  const int64_t lo = static_cast<int64_t>(a.rank) * a.shard;
+  const int64_t hi = (lo + a.shard < p) ? lo + a.shard : p;
+  float* mine = a.master[a.rank];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi; i += stride)
+    mine[i - lo] = i < nw ? W32[i] : b32[i - nw];
+}
+
+__global__ void k_colsum_push(const float* __restrict__ ws, int chunks, const AsyncLayer a, float lr, int coded,
+                              Round16 r16) {
+  __shared__ float sm[8][33];
+  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t cols = a.out;
+  const int64_t c = blockIdx.x * 32LL + cl;
+  float t = 0.f;
+  if (c < cols) {  // the same fixed summation order as k_colsum_final
+    int k = g;
+    for (; k + 24 < chunks; k += 32) {
+      const float a0 = ws[(int64_t)k * cols + c], a1 = ws[(int64_t)(k + 8) * cols + c];
+      const float a2 = ws[(int64_t)(k + 16) * cols + c], a3 = ws[(int64_t)(k + 24) * cols + c];
+      t = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(t, a0), a1), a2), a3);
+    }
+    for (; k < chunks; k += 8) t = __fadd_rn(t, ws[(int64_t)k * cols + c]);
+  }
+  sm[g][cl] = t;
+  __syncthreads();
+  if (g == 0 && c < cols) {
+    float s = sm[0][cl];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
+    const int64_t idx = a.in * a.out + c;
+    const int owner = static_cast<int>(idx / a.shard);
+    const float gh = (coded && owner != a.rank) ? __uint_as_float(round16(__float_as_uint(s), idx, r16) << 16) : s;
+    red_add_sys(a.master[owner] + (idx - static_cast<int64_t>(owner) * a.shard), -__fmul_rn(lr, gh));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_async_pull(const AsyncLayer& a, float* W32, float* b32, __nv_bfloat16* wop, int64_t ldwb,
+                              cudaStream_t s) {
+  k_async_pull<<<grid_for(a.in * a.out + a.out), 256, 0, s>>>(a, W32, b32, wop, ldwb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colsum_push(const float* ws, int chunks, const AsyncLayer& a, float lr, int coded, Round16 r,
+                               cudaStream_t s) {
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (a.out + 31) / 32));
+  k_colsum_push<<<blocks, 256, 0, s>>>(ws, chunks, a, lr, coded, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_async_publish(const AsyncLayer& a, const float* W32, const float* b32, cudaStream_t s) {
+  k_async_publish<<<grid_for(a.shard), 256, 0, s>>>(a, W32, b32);
+  return cudaGetLastError();
+}
+
+}  // namespace dflow

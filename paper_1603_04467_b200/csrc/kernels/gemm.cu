@@ -88,6 +88,8 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi, int* smem) {
     if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16>(smem);
     if (epi == EPI_SGD_APPLY) return kernel_ptr<BN, CG, TF32, true, true, EPI_SGD_APPLY>(smem);
     if (epi == EPI_TRUNC16_P2P) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16_P2P>(smem);
+    if constexpr (!TF32)
+      if (epi == EPI_ASYNC_PUSH) return kernel_ptr<BN, CG, TF32, true, true, EPI_ASYNC_PUSH>(smem);
   }
   return nullptr;
 }
@@ -218,6 +220,18 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
       return cudaErrorInvalidValue;
     }
     for (int r = 0; r < d.p2p_world; ++r) a.p2p_recv[r] = d.p2p_recv[r];
+    a.p2p_shard = d.p2p_shard;
+    a.p2p_rank = d.p2p_rank;
+    a.p2p_world = d.p2p_world;
+  }
+  if (d.epilogue == EPI_ASYNC_PUSH) {
+    if (!d.async_master || d.p2p_world < 1 || d.p2p_world > kMaxRanks || d.p2p_shard <= 0 || d.p2p_shard % 8 ||
+        d.p2p_rank < 0 || d.p2p_rank >= d.p2p_world || tf) {
+      snprintf(g_err, sizeof g_err, "bad asynchronous push arguments (bf16 path only)");
+      return cudaErrorInvalidValue;
+    }
+    for (int r = 0; r < d.p2p_world; ++r) a.async_master[r] = d.async_master[r];
+    a.async_coded = d.async_coded;
     a.p2p_shard = d.p2p_shard;
     a.p2p_rank = d.p2p_rank;
     a.p2p_world = d.p2p_world;

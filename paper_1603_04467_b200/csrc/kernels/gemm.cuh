@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "async_dp.h"
 #include "gemm.h"
 #include "ptx.cuh"
 
@@ -578,6 +579,38 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
             __syncwarp();
+          }
+        } else if constexpr (EPI == EPI_ASYNC_PUSH) {
+          // f3: this replica's update of element (m, n) lands in its owner's shard
+          // (reading A30: coded when another rank owns it; A31: one reduction, -fl(lr * g_hat))
+          if (active) {
+            const int64_t ib = static_cast<int64_t>(gm) * args.N + gn;  // bucket position of column gn
+            const int64_t shard = args.p2p_shard;
+            auto delta = [&](int j, int owner) {
+              const float g = u32_as_f32(r[j]);
+              const float gh = (args.async_coded && owner != args.p2p_rank)
+                                   ? __uint_as_float(round16(r[j], static_cast<uint64_t>(ib + j), args.r16) << 16)
+                                   : g;
+              return -__fmul_rn(args.sgd_lr, gh);
+            };
+            if (full_chunk && (args.N % 4) == 0) {
+              // 4 consecutive elements share an owner (shard % 8 == 0, ib % 4 == 0): one v4 reduction
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const int64_t idx = ib + j;
+                const int owner = static_cast<int>(idx / shard);
+                float* dst = args.async_master[owner] + (idx - static_cast<int64_t>(owner) * shard);
+                red_add_sys_v4(dst, delta(j, owner), delta(j + 1, owner), delta(j + 2, owner), delta(j + 3, owner));
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (gn + j >= args.N) continue;
+                const int64_t idx = ib + j;
+                const int owner = static_cast<int>(idx / shard);
+                red_add_sys(args.async_master[owner] + (idx - static_cast<int64_t>(owner) * shard), delta(j, owner));
+              }
+            }
           }
         } else if constexpr (EPI == EPI_SGD_APPLY) {
           // N = 1: ApplyGradientDescent fused into the dW epilogue (a4 + a9):

@@ -20,6 +20,8 @@ enum GemmEpilogue : int {
   EPI_SGD_APPLY = 5,       // out_f32 (fp32 master W) -= lr * acc; operand copy refreshed  (a4 + a9, N = 1)
   EPI_TRUNC16_P2P = 6,     // bits(acc) >> 16 stored straight into the OWNER rank's receive slot over
                            // NVLink (peer pointers): a4 + a6 + the all-to-all leg of a7 in one kernel
+  EPI_ASYNC_PUSH = 7,      // f3: owner's shard[m*N + n] += -fl(lr * g_hat) by a system-scope fp32
+                           // reduction over NVLink (g_hat coded when the owner is another rank)
 };
 
 constexpr int kMaxRanks = 8;
@@ -67,6 +69,10 @@ struct GemmArgs {
   // EPI_TRUNC16 / EPI_TRUNC16_P2P: the 16-bit code of element (m, n) is
   // round16(bits, m*N + n, r16) — truncation, or SR16 (reading A26)
   Round16 r16;
+  // EPI_ASYNC_PUSH: every rank's shard of the layer bucket (shard/rank/world in p2p_*, lr in
+  // sgd_lr); async_coded = 0 for the FP32 channel
+  float* async_master[kMaxRanks];
+  int async_coded;
 };
 
 struct GemmDesc {
@@ -85,6 +91,8 @@ struct GemmDesc {
   float* colsum_ws;                         // fused db partials (RELUGRAD, BIAS_RELU_LOSS)
   float sgd_lr;                             // EPI_SGD_APPLY
   uint16_t* const* p2p_recv;                // EPI_TRUNC16_P2P: [world] peer receive bases
+  float* const* async_master;               // EPI_ASYNC_PUSH: [world] shard bases
+  int async_coded;
   int64_t p2p_shard;
   int p2p_rank, p2p_world;
   int group;       // tile-raster group (M tiles); 0 = default

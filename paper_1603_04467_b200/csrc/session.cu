@@ -51,6 +51,10 @@ namespace {
 
 inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+int tbegin(dflow_session* s, int kind, cudaStream_t st);
+void tend(dflow_session* s, int idx, cudaStream_t st);
+dflow_status check_launch(dflow_session* s, cudaError_t e, int count, const char* what);
+
 // Gradients cross the channel as 16-bit codes (TRUNC16 or SR16).
 inline bool u16_wire(const dflow_session* s) {
   return s->opt.exchange == DFLOW_EXCHANGE_TRUNC16 || s->opt.exchange == DFLOW_EXCHANGE_SR16;
@@ -179,17 +183,24 @@ dflow_status match_graph(dflow_session* s) {
     if (ap.op != Op::ApplyGradientDescent) continue;
     int gid = ap.inputs[1];
     std::vector<int> chain;
-    if (xchg && u16_wire(s)) {
+    if (xchg && s->async && !u16_wire(s)) {
+      // asynchronous FP32 channel: the replica's gradient feeds its apply directly
+    } else if (xchg && u16_wire(s)) {
       const bool sr = s->opt.exchange == DFLOW_EXCHANGE_SR16;
       const int e = gid;
       if (g.nodes[e].op != Op::Expand16) return fail(DFLOW_UNIMPLEMENTED, "planner: missing Expand16 before apply");
-      const int m = g.nodes[e].inputs[0];
-      if (g.nodes[m].op != (sr ? Op::CrossReplicaMeanSR16 : Op::CrossReplicaMeanT16))
-        return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
-      const int t = g.nodes[m].inputs[0];
+      int m = g.nodes[e].inputs[0];
+      if (!s->async) {  // synchronous: the cross-replica mean sits between the code and the expand
+        if (g.nodes[m].op != (sr ? Op::CrossReplicaMeanSR16 : Op::CrossReplicaMeanT16))
+          return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
+        chain.push_back(m);
+        m = g.nodes[m].inputs[0];
+      }
+      const int t = m;
       if (g.nodes[t].op != (sr ? Op::StochasticRound16 : Op::Truncate16))
         return fail(DFLOW_UNIMPLEMENTED, "planner: missing the 32->16 coding node");
-      chain = {e, m, t};
+      chain.push_back(e);
+      chain.push_back(t);
       gid = g.nodes[t].inputs[0];
     } else if (xchg) {
       if (g.nodes[gid].op != Op::CrossReplicaMean) return fail(DFLOW_UNIMPLEMENTED, "planner: missing exchange");
@@ -291,14 +302,14 @@ dflow_status alloc_state(dflow_session* s) {
     ly.shard = ly.Ppad / N;
     ST(dmalloc(s, &ly.g32, ly.Ppad));
     ST(dmalloc(s, &ly.colsum_ws, ((cap + 31) / 32) * ly.out));
-    if (N > 1 && u16_wire(s) && !s->p2p) {
+    if (N > 1 && u16_wire(s) && !s->p2p && !s->async) {
       ST(dmalloc(s, &ly.q16, ly.Ppad));
       uint16_t *r, *o, *gt;
       ST(dmalloc(s, &r, ly.Ppad));
       ST(dmalloc(s, &o, ly.shard));
       ST(dmalloc(s, &gt, ly.Ppad));
       ly.recv = r; ly.own = o; ly.gath = gt;
-    } else if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_FP32) {
+    } else if (N > 1 && s->opt.exchange == DFLOW_EXCHANGE_FP32 && !s->async) {
       float *r, *o, *gt;
       ST(dmalloc(s, &r, ly.Ppad));
       ST(dmalloc(s, &o, ly.shard));
@@ -398,6 +409,55 @@ dflow_status setup_p2p(dflow_session* s) {
   return DFLOW_OK;
 }
 
+// Asynchronous replicas (f3): every rank allocates its fp32 shard of every layer bucket in
+// one symmetric allocation and maps every peer's through CUDA IPC (the same handle
+// exchange as setup_p2p).  Shards start zeroed; dflow_variable_assign publishes them.
+dflow_status setup_async(dflow_session* s) {
+  const int N = s->opt.world, R = s->opt.rank;
+  std::vector<size_t> off(s->L);
+  size_t total = 0;
+  for (int l = 0; l < s->L; ++l) {
+    off[l] = total;
+    total += (s->layers[l].shard * sizeof(float) + 255) / 256 * 256;
+  }
+  CU(cudaMalloc(&s->sym, total));
+  CU(cudaMemset(s->sym, 0, total));
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, s->sym));
+  uint8_t* dev = nullptr;
+  CU(cudaMalloc(&dev, 64 * (N + 1)));
+  CU(cudaMemcpy(dev, &h, 64, cudaMemcpyHostToDevice));
+  NC(ncclAllGather(dev, dev + 64, 64, ncclUint8, s->nccl, s->comm));
+  CU(cudaStreamSynchronize(s->comm));
+  std::vector<cudaIpcMemHandle_t> all(N);
+  CU(cudaMemcpy(all.data(), dev + 64, 64 * N, cudaMemcpyDeviceToHost));
+  cudaFree(dev);
+  for (int j = 0; j < N; ++j) {
+    if (j == R) s->peer_sym[j] = s->sym;
+    else CU(cudaIpcOpenMemHandle(&s->peer_sym[j], all[j], cudaIpcMemLazyEnablePeerAccess));
+  }
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    for (int j = 0; j < N; ++j) ly.async.master[j] = reinterpret_cast<float*>(static_cast<char*>(s->peer_sym[j]) + off[l]);
+    ly.async.shard = ly.shard;
+    ly.async.in = ly.in;
+    ly.async.out = ly.out;
+    ly.async.rank = R;
+    ly.async.world = N;
+  }
+  return DFLOW_OK;
+}
+
+dflow_status async_pull(dflow_session* s, cudaStream_t st) {
+  for (Layer& ly : s->layers) {
+    const int t = tbegin(s, 1, st);
+    cudaError_t e = launch_async_pull(ly.async, ly.W32, ly.b32, static_cast<__nv_bfloat16*>(ly.Wop.hi), ly.ld_wb, st);
+    tend(s, t, st);
+    ST(check_launch(s, e, 1, "parameter pull"));
+  }
+  return DFLOW_OK;
+}
+
 dflow_status gemm_plan(dflow_session* s, const GemmDesc& d, GemmPlan* p) {
   cudaError_t e = gemm_prepare(d, s->num_sms, p);
   if (e != cudaSuccess) return fail(DFLOW_CUDA, "GEMM plan: %s", gemm_last_error());
@@ -479,7 +539,20 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       ST(gemm_plan(s, wa, &ly.wgrad_apply));
       ly.has_wgrad_apply = true;
     }
-    if (s->opt.world > 1 && u16_wire(s) && !s->p2p) {
+    if (s->async) {
+      // f3: the dW epilogue pushes -lr * g_hat into the owners' shards
+      GemmDesc wa = w;
+      wa.epilogue = EPI_ASYNC_PUSH;
+      wa.out_f32 = nullptr;
+      wa.async_master = ly.async.master;
+      wa.async_coded = u16_wire(s) ? 1 : 0;
+      wa.p2p_shard = ly.shard;
+      wa.p2p_rank = s->opt.rank;
+      wa.p2p_world = s->opt.world;
+      wa.sgd_lr = ly.n.lr_W;
+      ST(gemm_plan(s, wa, &ly.wgrad_async));
+    }
+    if (s->opt.world > 1 && u16_wire(s) && !s->p2p && !s->async) {
       w.epilogue = EPI_TRUNC16;
       w.out_f32 = nullptr;
       w.out = ly.q16; w.out2 = nullptr; w.ldo = ly.out;
@@ -700,6 +773,21 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
 
 // mode 0: train (TRUNC16 buckets + exchange + apply); 1: fetch (fp32 grads, no exchange)
 dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int mode) {
+  if (mode == 0 && s->async) {  // f3: push every layer's update into the owners' shards, no exchange
+    for (int l = s->L - 1; l >= 0; --l) {
+      Layer& ly = s->layers[l];
+      if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
+      const Round16 code = round16_of(s, l, 0);
+      ly.wgrad_async.args.r16 = code;
+      ST(launch_gemm(s, ly.wgrad_async, st));
+      const int t = tbegin(s, 1, st);
+      cudaError_t e = launch_colsum_push(ly.colsum_ws, static_cast<int>((rows + 31) / 32), ly.async, ly.n.lr_b,
+                                         u16_wire(s) ? 1 : 0, code, st);
+      tend(s, t, st);
+      ST(check_launch(s, e, 1, "bias-gradient push"));
+    }
+    return DFLOW_OK;
+  }
   const bool t16 = mode == 0 && s->opt.world > 1 && u16_wire(s);
   for (int l = s->L - 1; l >= 0; --l) {
     Layer& ly = s->layers[l];
@@ -751,7 +839,7 @@ cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st) {
 }
 
 dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
-  if (s->opt.world > 1) {
+  if (s->opt.world > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
     CU(cudaEventRecord(s->ev_loss, st));
     CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
     NC(ncclAllReduce(s->loss_dev, s->loss_dev + 1, 1, ncclFloat32, ncclSum, s->nccl, s->comm));
@@ -770,7 +858,7 @@ dflow_status wait_loss(dflow_session* s, float* loss_out) {
   s->loss_pending = false;
   CU(cudaEventSynchronize(s->ev_loss_ready));
   float v = s->loss_host[0];
-  if (s->opt.world > 1) v /= static_cast<float>(s->opt.world);
+  if (s->opt.world > 1 && !s->async) v /= static_cast<float>(s->opt.world);
   if (loss_out) *loss_out = v;
   s->nonfinite = std::isfinite(v) ? 0 : 1;
   return DFLOW_OK;
@@ -804,9 +892,20 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   s->cap = opt.max_local_rows;
   s->tf32 = opt.precision == DFLOW_PRECISION_3XTF32;
   s->esz = s->tf32 ? 4 : 2;
-  s->p2p = opt.p2p && opt.world > 1 &&
+  s->async = opt.async_dp != 0 && opt.world > 1;
+  if (s->async && (s->tf32 || !(opt.exchange == DFLOW_EXCHANGE_TRUNC16 || opt.exchange == DFLOW_EXCHANGE_SR16 ||
+                                 opt.exchange == DFLOW_EXCHANGE_FP32))) {
+    delete s;
+    return fail(DFLOW_INVALID_ARGUMENT, "async_dp needs the bf16 path and a TRUNC16, SR16 or FP32 channel");
+  }
+  if (s->async && opt.world > kMaxRanks) {
+    delete s;
+    return fail(DFLOW_INVALID_ARGUMENT, "async_dp supports up to %d ranks", kMaxRanks);
+  }
+  s->p2p = !s->async && opt.p2p && opt.world > 1 &&
            (opt.exchange == DFLOW_EXCHANGE_TRUNC16 || opt.exchange == DFLOW_EXCHANGE_SR16);
-  dflow_status st = insert_exchange(user, opt.world, opt.exchange, &s->g, &s->remap);
+  dflow_status st = insert_exchange(user, opt.world, opt.exchange | (s->async ? DFLOW_EXCHANGE_ASYNC : 0), &s->g,
+                                    &s->remap);
   if (st == DFLOW_OK) st = match_graph(s);
   if (st == DFLOW_OK && s->tf32 && s->x_dtype != DFLOW_F32)
     st = fail(DFLOW_INVALID_ARGUMENT, "the 3xTF32 path needs an fp32 x placeholder");
@@ -839,6 +938,7 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     if (r != ncclSuccess) st = fail(DFLOW_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
   }
   if (st == DFLOW_OK && s->p2p) st = setup_p2p(s);
+  if (st == DFLOW_OK && s->async) st = setup_async(s);
   if (st != DFLOW_OK) {
     session_destroy(s);
     return st;
@@ -893,6 +993,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   // one step's work on `stream` (also what a step graph captures)
   auto body = [&](cudaStream_t stream) -> dflow_status {
     s->launches = s->gemm_launches = 0;
+    if (s->async && s->opt.async_dp == 1) ST(async_pull(s, stream));  // the replica reads the shared parameters
     ST(run_forward(s, f, rows, stream, FWD_TRAIN));
     CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
     if (loss_out) ST(enqueue_loss(s, stream));
@@ -1110,6 +1211,7 @@ dflow_status session_variable_assign(dflow_session* s, dflow_node var, const voi
       return fail(DFLOW_CUDA, "weight cast: %s", cudaGetErrorString(e));
     }
   }
+  if (s->async) CU(launch_async_publish(ly.async, ly.W32, ly.b32, st));  // this rank's shard of the shared copy
   if (!on_dev) CU(cudaStreamSynchronize(st));
   return DFLOW_OK;
 }
@@ -1122,6 +1224,7 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
   if (l < 0) return fail(DFLOW_INVALID_ARGUMENT, "node is not a Variable of the planned MLP");
   cudaSetDevice(s->opt.device);
   Layer& ly = s->layers[l];
+  if (s->async) ST(async_pull(s, st));  // the shared parameters, not this replica's last pull
   const float* src = is_bias ? ly.b32 : ly.W32;
   const size_t bytes = (is_bias ? ly.out : ly.in * ly.out) * sizeof(float);
   if (on_dev) {
@@ -1131,6 +1234,13 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
     CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
   }
   return DFLOW_OK;
+}
+
+dflow_status session_async_pull(dflow_session* s, cudaStream_t st) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  if (!s->async) return fail(DFLOW_INVALID_ARGUMENT, "not an async_dp session");
+  cudaSetDevice(s->opt.device);
+  return async_pull(s, st);
 }
 
 dflow_status session_exchange(dflow_session* s, const float* grad, float* out, size_t n, cudaStream_t st) {

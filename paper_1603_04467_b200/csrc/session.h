@@ -10,6 +10,7 @@
 
 #include "../../include/dflow.h"
 #include "graph.h"
+#include "kernels/async_dp.h"
 #include "kernels/exchange_p2p.h"
 #include "kernels/gemm.h"
 
@@ -49,7 +50,8 @@ struct Layer {
   void* gath = nullptr;           // allgather landing [Ppad]
   float* colsum_ws = nullptr;     // fused db partials [ceil(cap/32), out]
   P2PLayer p2p;                   // fused NVLink exchange: peer pointers of this layer
-  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16, wgrad_apply, wgrad_p2p;
+  AsyncLayer async;               // asynchronous replicas (f3): every rank's shard of this layer
+  GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16, wgrad_apply, wgrad_p2p, wgrad_async;
   bool has_fwd = false, has_dgrad = false, has_wgrad16 = false, has_wgrad_apply = false, has_wgrad_p2p = false;
 };
 
@@ -116,6 +118,7 @@ struct dflow_session {
   ncclComm_t nccl = nullptr;
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;
+  bool async = false;  // opt.async_dp (f3): sym holds this rank's parameter shards
   void* sym = nullptr;
   void* peer_sym[dflow::kMaxRanks] = {};
   int* p2p_done = nullptr;
@@ -152,6 +155,7 @@ dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_
 dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_host);
 dflow_status session_variable_assign(dflow_session* s, dflow_node var, const void* src, int on_dev, cudaStream_t st);
 dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, int on_dev, cudaStream_t st);
+dflow_status session_async_pull(dflow_session* s, cudaStream_t st);
 dflow_status session_exchange(dflow_session* s, const float* grad, float* out, size_t n, cudaStream_t st);
 dflow_status session_stats(dflow_session* s, dflow_stats* out);
 }  // namespace dflow

@@ -149,6 +149,29 @@ def test_compression_pass_matches_oracle_pass(world, exchange):
         D.dflow_graph_destroy(m.graph)
 
 
+@pytest.mark.parametrize("world,exchange", [(2, "TRUNC16"), (4, "SR16"), (2, "FP32")])
+def test_async_compression_pass_matches_oracle_and_plans(world, exchange):
+    # f3: code -> expand -> apply per replica, no mean; the planner takes it
+    dims = (16, 8, 4)
+    mg = build_mlp(dims, "MSE", 0.5)
+    m = D.mlp_graph(dims, "MSE", 0.5)
+    out = C.c_void_p()
+    try:
+        D.check(D.dflow_graph_insert_exchange(m.graph, world, D.EXCHANGES[exchange] | 0x100, C.byref(out)))
+        ref = OG.insert_exchange(mg.graph, world, exchange, asynchronous=True)
+        assert _canon(D.graph_json(out)) == _canon(ref.to_json())
+        assert not any("mean" in n.name for n in ref.nodes)
+        opts = D.make_options(world=world, exchange=exchange, max_local_rows=8, async_dp=1)
+        s = C.c_void_p()
+        st = D.dflow_session_create(m.graph, C.byref(opts), (C.c_uint8 * 128)(), C.byref(s))
+        assert st in (D.DFLOW_OK, D.DFLOW_CUDA), D.dflow_last_error()  # never UNIMPLEMENTED
+        if st == D.DFLOW_OK:
+            D.dflow_session_destroy(s)
+    finally:
+        D.dflow_graph_destroy(out)
+        D.dflow_graph_destroy(m.graph)
+
+
 def test_round16_key_matches_the_oracle_key_derivation():
     # host code of the product vs the oracle's independent implementation (reading A27)
     from oracle.codec import sr_key

@@ -27,6 +27,10 @@ def _run(n, exchange, tmp_path):
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mgpu_worker.py"), str(out), exchange]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    log = r.stdout + r.stderr
+    if r.returncode != 0 and any(k in log for k in ("EADDRINUSE", "Address already in use", "DistNetworkError")):
+        cmd[cmd.index("--master-port") + 1] = str(_free_port())  # rendezvous port race: one retry
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     return json.load(open(out))
 
