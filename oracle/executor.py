@@ -18,6 +18,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import kernels as K
+from .codec import expand16, truncate16
 from .graph import Graph, GraphError, INVALID_ARGUMENT
 
 
@@ -105,6 +106,10 @@ def _run_node(graph, name, feeds, values, variables, mode, masks):
         return K.loss(n.attrs["kind"], ins[0], ins[1] if len(ins) > 1 else None, mode)
     if op == "LossGrad":
         return K.loss_grad(n.attrs["kind"], ins[0], ins[1] if len(ins) > 1 else None, mode)
+    if op == "Truncate16":  # channel codec (reading A5)
+        return truncate16(np.asarray(ins[0], np.float32))
+    if op == "Expand16":
+        return expand16(ins[0]) if mode == "f32" else expand16(ins[0]).astype(np.float64)
     if op == "ApplyGradientDescent":
         new = K.apply_gradient_descent(ins[0], n.attrs["lr"], ins[1], mode)
         variables[n.inputs[0]] = new

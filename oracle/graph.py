@@ -37,7 +37,9 @@ OPS = ("Placeholder", "Variable", "MatMul", "Add", "Relu", "Loss", "LossGrad", "
        # inserted by insert_exchange (the replicated graph's transfer nodes)
        "Truncate16", "CrossReplicaMeanT16", "Expand16", "CrossReplicaMean",
        # f2: the probabilistic-rounding variant of the same channel (reading A26)
-       "StochasticRound16", "CrossReplicaMeanSR16")
+       "StochasticRound16", "CrossReplicaMeanSR16",
+       # f4: cross-device channel endpoints of a partitioned graph
+       "Send", "Recv")
 BATCH = -1  # unknown (batch) dimension, only allowed through Placeholder
 _NAME_RE = re.compile(r"^[A-Za-z0-9_./]+$")
 
