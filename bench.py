@@ -189,10 +189,11 @@ def run_reference(args, w):
 def config_dict(w, args, world):
     return {"workload": w.name, "global_batch": w.batch, "layers": w.layers, "width": w.dims[1],
             "dims": list(w.dims), "loss": w.loss, "lr": w.lr,
-            "exchange": ("ASYNC_" if (world > 1 and getattr(args, "async_dp", 0)) else "") + args.exchange +
-                        ("_P2P" if (args.exchange in ("TRUNC16", "SR16") and world > 1 and getattr(args, "p2p", 0)
-                                    and not getattr(args, "async_dp", 0)) else ""),
-            "parallelism": f"dp{world}",
+            "exchange": ("SENDRECV_TRUNC16_CHANNELS" if (world > 1 and getattr(args, "model_parallel", 0)) else
+                         ("ASYNC_" if (world > 1 and getattr(args, "async_dp", 0)) else "") + args.exchange +
+                         ("_P2P" if (args.exchange in ("TRUNC16", "SR16") and world > 1 and getattr(args, "p2p", 0)
+                                     and not getattr(args, "async_dp", 0)) else "")),
+            "parallelism": (f"mp{world}" if (world > 1 and getattr(args, "model_parallel", 0)) else f"dp{world}"),
             "precision": ("3xTF32 split fp32 operands (big, small), fp32 accumulate + master weights"
                           if w.precision == "3xtf32" else "bf16 operands, fp32 accumulate + master weights"),
             "l2": ("no flush: every step streams inputs and activations far larger than the 126 MB L2 "
@@ -214,7 +215,9 @@ def run_gpu(args, w):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1603_04467_b200 as D
 
-    row0, b = shard_rows(w.batch, world, rank)
+    mp = world > 1 and getattr(args, "model_parallel", 0)
+    # model parallelism (f4): one replica, every rank steps the whole batch through its layers
+    row0, b = (0, w.batch) if mp else shard_rows(w.batch, world, rank)
     # NCCL id from rank 0, broadcast through torch.distributed (plumbing only)
     nid = None
     if world > 1:
@@ -224,6 +227,7 @@ def run_gpu(args, w):
     opts = D.make_options(world=world, rank=rank, device=local, exchange=args.exchange, max_local_rows=b,
                           overlap=1, sm_reserve=args.sm_reserve, p2p=args.p2p, sr_seed=1234,
                           graphs=1 if world == 1 else 0, async_dp=args.async_dp if world > 1 else 0,
+                          model_parallel=1 if mp else 0,
                           precision=D.DFLOW_PRECISION_3XTF32 if tf32 else D.DFLOW_PRECISION_BF16)
     s = D.session_create(mlp, opts, nid)
     Ws, bs = synth.init_params(w)
@@ -368,6 +372,10 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="override the global batch (parity/debug only)")
     ap.add_argument("--exchange", default="TRUNC16", choices=["TRUNC16", "FP32", "FP32_NCCL", "NONE", "SR16"])
+    ap.add_argument("--model-parallel", type=int, default=0,
+                    help="N > 1: 1 = layer-wise model parallelism (f4): rank r holds layers "
+                         "[r L / N, (r+1) L / N), activations / their gradients cross through Send/Recv "
+                         "with the 16-bit channel codec")
     ap.add_argument("--async-dp", type=int, default=0,
                     help="N > 1: 1 = asynchronous replicas (f3): each rank pulls the shared parameters, steps "
                          "and pushes its own coded update with no barrier (the exchange names the coding)")

@@ -110,6 +110,15 @@ dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, si
  * every node of g in *out only through dflow_node_by_name.                       */
 dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int exchange, dflow_graph** out);
 
+/* Partition pass (f4): device_of_node[i] (n_nodes = every node of g, in
+ * id order) places node i; *out receives device `device`'s subgraph, in which every
+ * cross-device edge x -> y is replaced by Recv [-> Expand16] (one per endpoint and
+ * destination, shared by all its consumers there) and the producers' side gets
+ * [Truncate16 ->] Send (compress = 1: the channel codec of PAPER.md:813-821, reading A33).
+ * Send/Recv carry tensor_name, send_device, recv_device.  Caller owns *out.           */
+dflow_status dflow_graph_partition(const dflow_graph* g, const int32_t* device_of_node, int32_t n_nodes, int32_t device,
+                                   int32_t compress, dflow_graph** out);
+
 /* ---------------------------------------------------------------- session
  * One session per (rank, GPU).  dflow_session_create copies the graph (an
  * immutable snapshot), runs the replication + compression-insertion pass and
@@ -148,6 +157,13 @@ typedef struct {
                              A29-A31; exchange TRUNC16 / SR16 / FP32 = the coding of the
                              cross-device pushes); 2 = the same without the automatic pull
                              (the client calls dflow_async_pull)                             */
+  int32_t model_parallel; /* world > 1, bf16: 1 = layer-wise model parallelism (f4):
+                             one replica; rank r holds layers [floor(r L / N), floor((r+1) L / N))
+                             (reading A32), the activation crossing to the next rank and the
+                             gradient crossing back travel through Send/Recv with the 16-bit
+                             channel codec (A33); every rank applies its own layers' updates.
+                             Every rank calls dflow_train_step with the full batch (x used
+                             on rank 0, y on the last rank); the loss is broadcast.         */
   int32_t graphs;         /* world == 1: 1 = capture the train step into a CUDA graph per feed
                              signature (x, y pointers, leading dims, rows) and replay it — one
                              launch per step instead of ~4L host launches (latency-bound C2);

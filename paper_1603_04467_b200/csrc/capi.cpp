@@ -181,6 +181,23 @@ dflow_status dflow_graph_to_json(const dflow_graph* g, char* buf, size_t cap, si
   GUARD_END
 }
 
+dflow_status dflow_graph_partition(const dflow_graph* g, const int32_t* device_of_node, int32_t n_nodes, int32_t device,
+                                   int32_t compress, dflow_graph** out) {
+  GUARD_BEGIN
+  if (!g || !device_of_node || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
+  if (n_nodes != static_cast<int32_t>(g->g.nodes.size())) return fail(DFLOW_INVALID_ARGUMENT, "n_nodes != node count");
+  std::vector<int> place(device_of_node, device_of_node + n_nodes);
+  std::vector<dflow::Graph> parts;
+  dflow_status st = dflow::partition(g->g, place, compress != 0, &parts);
+  if (st != DFLOW_OK) return st;
+  if (device < 0 || device >= static_cast<int32_t>(parts.size())) return fail(DFLOW_INVALID_ARGUMENT, "no such device");
+  dflow_graph* r = new dflow_graph();
+  r->g = std::move(parts[device]);
+  *out = r;
+  return DFLOW_OK;
+  GUARD_END
+}
+
 dflow_status dflow_graph_insert_exchange(const dflow_graph* g, int world, int exchange, dflow_graph** out) {
   GUARD_BEGIN
   if (!g || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");

@@ -3,6 +3,8 @@
 #include "graph.h"
 
 #include <algorithm>
+#include <map>
+#include <string>
 #include <cstdio>
 #include <cstring>
 
@@ -30,6 +32,8 @@ const char* op_name(Op op) {
     case Op::CrossReplicaMean: return "CrossReplicaMean";
     case Op::StochasticRound16: return "StochasticRound16";
     case Op::CrossReplicaMeanSR16: return "CrossReplicaMeanSR16";
+    case Op::Send: return "Send";
+    case Op::Recv: return "Recv";
   }
   return "?";
 }
@@ -401,6 +405,13 @@ std::string Graph::to_json() const {
         snprintf(buf, sizeof buf, "\"world\": %d", n.world);
         o += buf;
         break;
+      case Op::Send:
+      case Op::Recv:
+        snprintf(buf, sizeof buf, "\"recv_device\": %d, \"send_device\": %d, \"tensor_name\": ", n.recv_device,
+                 n.send_device);
+        o += buf;
+        json_str(o, n.tensor_name);
+        break;
       default:
         break;
     }
@@ -487,6 +498,80 @@ dflow_status insert_exchange(const Graph& in, int world, int exchange, Graph* ou
     dflow_status st = out->append(std::move(n), &nid);
     if (st) return st;
     (*remap)[i] = nid;
+  }
+  return DFLOW_OK;
+}
+
+// ------------------------------------------------------------------ partition pass (f4)
+dflow_status partition(const Graph& in, const std::vector<int>& place, bool compress, std::vector<Graph>* out) {
+  const int n = static_cast<int>(in.nodes.size());
+  if (static_cast<int>(place.size()) != n) return fail(DFLOW_INVALID_ARGUMENT, "placement size != node count");
+  int ndev = 0;
+  for (int d : place) {
+    if (d < 0) return fail(DFLOW_INVALID_ARGUMENT, "negative device in the placement");
+    ndev = std::max(ndev, d + 1);
+  }
+  out->assign(ndev, Graph());
+  std::vector<std::vector<int>> local(ndev, std::vector<int>(n, -1));
+  std::map<std::pair<int, int>, int> chan;  // (endpoint, destination) -> node providing it there
+  for (int i = 0; i < n; ++i) {
+    const int d = place[i];
+    Node nd = in.nodes[i];
+    for (int& k : nd.inputs) {
+      const int src = place[k];
+      if (src == d) {
+        k = local[d][k];
+        continue;
+      }
+      auto it = chan.find({k, d});
+      if (it == chan.end()) {
+        const Node& x = in.nodes[k];
+        const std::string key = x.name + "/" + std::to_string(src) + "to" + std::to_string(d);
+        int id = local[src][k];
+        dflow_status st;
+        if (compress) {
+          Node t;
+          t.name = "chan/" + key + "/trunc16";
+          t.op = Op::Truncate16;
+          t.inputs = {id};
+          t.dtype = DFLOW_U16;
+          t.shape = x.shape;
+          if ((st = (*out)[src].append(t, &id))) return st;
+        }
+        Node s;
+        s.name = "send/" + key;
+        s.op = Op::Send;
+        s.inputs = {id};
+        s.dtype = compress ? DFLOW_U16 : DFLOW_F32;
+        s.shape = x.shape;
+        s.tensor_name = x.name;
+        s.send_device = src;
+        s.recv_device = d;
+        int sid;
+        if ((st = (*out)[src].append(s, &sid))) return st;
+        Node r = s;
+        r.name = "recv/" + key;
+        r.op = Op::Recv;
+        r.inputs.clear();
+        int rid;
+        if ((st = (*out)[d].append(r, &rid))) return st;
+        if (compress) {
+          Node e;
+          e.name = "chan/" + key + "/expand16";
+          e.op = Op::Expand16;
+          e.inputs = {rid};
+          e.dtype = DFLOW_F32;
+          e.shape = x.shape;
+          if ((st = (*out)[d].append(e, &rid))) return st;
+        }
+        it = chan.emplace(std::make_pair(k, d), rid).first;
+      }
+      k = it->second;
+    }
+    int id;
+    dflow_status st = (*out)[d].append(std::move(nd), &id);
+    if (st) return st;
+    local[d][i] = id;
   }
   return DFLOW_OK;
 }

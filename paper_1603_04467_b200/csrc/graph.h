@@ -31,6 +31,8 @@ enum class Op : int {
   CrossReplicaMean,
   StochasticRound16,     // SR16 (f2)
   CrossReplicaMeanSR16,
+  Send,                  // f4: cross-device channel endpoints
+  Recv,
 };
 
 const char* op_name(Op op);
@@ -46,6 +48,8 @@ struct Node {
   float lr = 0.f;                         // ApplyGradientDescent
   int axis = -1;                          // ReduceSum
   int world = 0;                          // exchange nodes
+  std::string tensor_name;                // Send / Recv: the transferred endpoint
+  int send_device = -1, recv_device = -1;  // Send / Recv
 };
 
 class Graph {
@@ -83,5 +87,12 @@ class Graph {
 // world == 1 or exchange NONE: the graph is copied unchanged (reading A6).
 // `remap[old_id] = new_id`.
 dflow_status insert_exchange(const Graph& in, int world, int exchange, Graph* out, std::vector<int>* remap);
+
+// Partition pass (f4): place[i] = device of node i.  Every cross-device
+// edge x -> y becomes x -> [Truncate16 ->] Send in x's subgraph and Recv [-> Expand16] -> y
+// in y's, one channel per (x, destination device) shared by all consumers there
+// (canonicalisation); compress = the channel codec of PAPER.md:813-821.  out[d] = device
+// d's subgraph, nodes in construction order.
+dflow_status partition(const Graph& in, const std::vector<int>& place, bool compress, std::vector<Graph>* out);
 
 }  // namespace dflow

@@ -223,6 +223,27 @@ __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t
   }
 }
 
+// ------------------------------------------------------------------ f4 channel (backward)
+// block: 32 x 8 threads = 256 columns x one 32-row chunk; each thread one column, rows in order
+__global__ void k_relugrad_recv(const uint16_t* __restrict__ code, int64_t ldc, const __nv_bfloat16* __restrict__ a,
+                                int64_t lda, int64_t rows, int64_t cols, __nv_bfloat16* __restrict__ dz, int64_t ldz,
+                                float* __restrict__ colsum_ws) {
+  const int64_t c = blockIdx.x * 256LL + threadIdx.y * 32 + threadIdx.x;
+  const int64_t r0 = blockIdx.y * 32LL;
+  if (c >= cols) return;
+  const uint16_t* ab = reinterpret_cast<const uint16_t*>(a);
+  uint16_t* zb = reinterpret_cast<uint16_t*>(dz);
+  float sum = 0.f;
+  for (int64_t r = r0; r < r0 + 32 && r < rows; ++r) {
+    const uint32_t h = ab[r * lda + c];
+    const bool pos = (h & 0x8000u) == 0 && h != 0 && h <= 0x7F80u;  // a > 0 (bf16 bits)
+    const uint16_t q = pos ? code[r * ldc + c] : 0;
+    zb[r * ldz + c] = q;
+    sum = __fadd_rn(sum, __uint_as_float(static_cast<uint32_t>(q) << 16));
+  }
+  colsum_ws[blockIdx.y * cols + c] = sum;
+}
+
 // ------------------------------------------------------------------ owner reduce
 __global__ void k_owner_reduce_t16(const uint16_t* __restrict__ recv, int64_t shard, int nranks,
                                    uint16_t* __restrict__ out, Round16 r16, int64_t idx_base) {
@@ -442,6 +463,14 @@ cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nra
                                     cudaStream_t s, Round16 r, int64_t idx_base) {
   if (shard == 0) return cudaSuccess;
   k_owner_reduce_t16<<<blocks_for(shard / 8), kThreads, 0, s>>>(recv, shard, nranks, out, r, idx_base);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relugrad_recv(const uint16_t* code, int64_t ldc, const __nv_bfloat16* a, int64_t lda, int64_t rows,
+                                 int64_t cols, __nv_bfloat16* dz, int64_t ldz, float* colsum_ws, cudaStream_t s) {
+  if (rows * cols == 0) return cudaSuccess;
+  const dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + 31) / 32));
+  k_relugrad_recv<<<grid, dim3(32, 8), 0, s>>>(code, ldc, a, lda, rows, cols, dz, ldz, colsum_ws);
   return cudaGetLastError();
 }
 

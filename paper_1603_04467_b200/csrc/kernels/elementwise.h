@@ -57,6 +57,12 @@ cudaError_t launch_apply_sgd(float* W, const float* g32, const uint16_t* g16, in
 cudaError_t launch_apply_sgd_tf32(float* W, const float* g32, const uint16_t* g16, int64_t rows, int64_t cols,
                                   float* whi, float* wlo, int64_t ldw, float lr, cudaStream_t s);
 
+// f4 (model parallelism), the receiving end of the backward channel: dz = expand(code) where
+// this rank's activation a > 0, else 0 (ReluGrad on the received dA, reading A33), stored
+// bf16 [rows, ldz]; also the per-32-row column partial sums of dz ([ceil(rows/32), cols]).
+cudaError_t launch_relugrad_recv(const uint16_t* code, int64_t ldc, const __nv_bfloat16* a, int64_t lda, int64_t rows,
+                                 int64_t cols, __nv_bfloat16* dz, int64_t ldz, float* colsum_ws, cudaStream_t s);
+
 // Bit-pack 1[a > 0] of a bf16 [rows, ld] activation (cols columns) row-major.
 cudaError_t launch_relu_mask_bits(const __nv_bfloat16* a, int64_t ld, int64_t rows, int64_t cols, uint32_t* bits,
                                   cudaStream_t s);

@@ -83,6 +83,8 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi, int* smem) {
   } else if (!a_mn && !b_mn) {  // dgrad: dZ K-major, W K-major
     if (epi == EPI_RELUGRAD) return kernel_ptr<BN, CG, TF32, false, false, EPI_RELUGRAD>(smem);
     if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, false, false, EPI_F32>(smem);
+    if constexpr (!TF32)  // f4: dA leaving for the previous rank as channel codes
+      if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, false, false, EPI_TRUNC16>(smem);
   } else if (a_mn && b_mn) {  // wgrad: activations and dZ both MN-major
     if (epi == EPI_F32) return kernel_ptr<BN, CG, TF32, true, true, EPI_F32>(smem);
     if (epi == EPI_TRUNC16) return kernel_ptr<BN, CG, TF32, true, true, EPI_TRUNC16>(smem);
@@ -213,6 +215,7 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.seed_const = 1.0f / static_cast<float>(d.M);
   a.loss_partials = d.loss_partials;
   a.colsum_ws = d.colsum_ws;
+  a.trunc_out = d.trunc_out;
   if (d.epilogue == EPI_TRUNC16_P2P) {
     if (!d.p2p_recv || d.p2p_world < 1 || d.p2p_world > kMaxRanks || d.p2p_shard <= 0 || d.p2p_shard % 8 ||
         d.p2p_rank < 0 || d.p2p_rank >= d.p2p_world) {

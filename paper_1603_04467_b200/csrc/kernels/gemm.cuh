@@ -104,11 +104,14 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // value, or the exact fp32 value (= big + small) in the 3xTF32 path.
 template <bool TF32>
 __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, void* lo_base, int64_t ld, int64_t gm,
-                                              int gn, int N, bool vec) {
+                                              int gn, int N, bool vec, bool trunc = false) {
   const bool full = gn + 32 <= N;
   if constexpr (!TF32) {
+    // bf16 operand: RNE (reading A19), or — where the tensor crosses a device (f4 channel,
+    // reading A33) — the channel's 16-bit truncation code, which is a bf16 bit pattern
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+    for (int j = 0; j < 32; ++j)
+      v[j] = trunc ? __uint_as_float(__float_as_uint(v[j]) & 0xFFFF0000u) : __bfloat162float(__float2bfloat16_rn(v[j]));
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(hi_base) + gm * ld + gn;
     if (full && vec) {
 #pragma unroll
@@ -673,7 +676,8 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
             if (args.out != nullptr)
-              store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0);
+              store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0,
+                                  args.trunc_out != 0);
           }
         } else if constexpr (EPI == EPI_RELUGRAD || EPI == EPI_BIAS_RELU_LOSS) {
           // dz values as stored, 0 outside the matrix; fused db column sums.

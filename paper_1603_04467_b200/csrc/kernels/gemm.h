@@ -73,6 +73,9 @@ struct GemmArgs {
   // sgd_lr); async_coded = 0 for the FP32 channel
   float* async_master[kMaxRanks];
   int async_coded;
+  // EPI_BIAS_RELU: 1 = store the operand as the channel's 16-bit truncation code instead of
+  // the RNE bf16 value (f4: the activation that crosses to the next device, reading A33)
+  int trunc_out;
 };
 
 struct GemmDesc {
@@ -93,6 +96,7 @@ struct GemmDesc {
   uint16_t* const* p2p_recv;                // EPI_TRUNC16_P2P: [world] peer receive bases
   float* const* async_master;               // EPI_ASYNC_PUSH: [world] shard bases
   int async_coded;
+  int trunc_out;                            // EPI_BIAS_RELU: truncation code instead of RNE
   int64_t p2p_shard;
   int p2p_rank, p2p_world;
   int group;       // tile-raster group (M tiles); 0 = default

@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <set>
+#include <tuple>
 
 #include "common.h"
 #include "kernels/elementwise.h"
@@ -176,7 +178,7 @@ dflow_status match_graph(dflow_session* s) {
     }
   }
   // ApplyGradientDescent nodes, through the exchange chain the compression pass inserted
-  const bool xchg = s->opt.world > 1 && s->opt.exchange != DFLOW_EXCHANGE_NONE;
+  const bool xchg = s->replicas > 1 && s->opt.exchange != DFLOW_EXCHANGE_NONE;
   int applies = 0;
   for (int i = 0; i < n; ++i) {
     const Node& ap = g.nodes[i];
@@ -282,8 +284,48 @@ cudaError_t to_operand(dflow_session* s, const float* src, int64_t lds, const Op
   return launch_cast_bf16(src, lds, static_cast<__nv_bfloat16*>(op.hi), ldd, rows, cols, st);
 }
 
+// f4: layer-wise placement (reading A32) and the check that the partition pass puts the
+// channels exactly where the runtime implements them: per boundary, the activation forward
+// and its gradient (dA) backward, both through the 16-bit codec (A33).
+dflow_status setup_mp(dflow_session* s) {
+  const int N = s->opt.world, L = s->L, R = s->opt.rank;
+  if (N > L) return fail(DFLOW_INVALID_ARGUMENT, "model_parallel needs at least as many layers (%d) as ranks (%d)", L, N);
+  auto dev = [&](int l) { return (l * N) / L; };
+  std::vector<int> place(s->g.nodes.size(), -1);
+  for (int l = 0; l < L; ++l) {
+    const LayerNodes& n = s->layers[l].n;
+    for (int id : {n.W, n.b, n.mm, n.add, n.relu, n.relugrad, n.db, n.dW, n.dX, n.apply_W, n.apply_b})
+      if (id >= 0) place[id] = dev(l);
+  }
+  place[s->x] = 0;
+  for (int id : {s->y, s->cost, s->lossgrad})
+    if (id >= 0) place[id] = dev(L - 1);
+  for (size_t i = 0; i < place.size(); ++i)
+    if (place[i] < 0) return fail(DFLOW_UNIMPLEMENTED, "model_parallel: node '%s' has no placement", s->g.nodes[i].name.c_str());
+  std::vector<Graph> parts;
+  ST(partition(s->g, place, true, &parts));
+  std::set<std::tuple<std::string, int, int>> got, want;
+  for (const Graph& g : parts)
+    for (const Node& n : g.nodes)
+      if (n.op == Op::Send) got.insert(std::make_tuple(n.tensor_name, n.send_device, n.recv_device));
+  for (int l = 1; l < L; ++l) {
+    if (dev(l) == dev(l - 1)) continue;
+    want.insert(std::make_tuple(s->g.nodes[s->layers[l - 1].n.relu].name, dev(l - 1), dev(l)));
+    if (s->layers[l].n.dX >= 0) want.insert(std::make_tuple(s->g.nodes[s->layers[l].n.dX].name, dev(l), dev(l - 1)));
+  }
+  if (got != want) return fail(DFLOW_UNIMPLEMENTED, "model_parallel: the partition's channels are not the MLP's boundary pair");
+  s->mp_lo = L;
+  s->mp_hi = 0;
+  for (int l = 0; l < L; ++l)
+    if (dev(l) == R) {
+      s->mp_lo = std::min(s->mp_lo, l);
+      s->mp_hi = std::max(s->mp_hi, l + 1);
+    }
+  return DFLOW_OK;
+}
+
 dflow_status alloc_state(dflow_session* s) {
-  const int N = s->opt.world;
+  const int N = s->replicas;
   const int64_t cap = s->cap;
   s->ld_A0 = pad_to(s->layers[0].in, 8);
   ST(alloc_operand(s, &s->A0, cap * s->ld_A0));
@@ -466,7 +508,7 @@ dflow_status gemm_plan(dflow_session* s, const GemmDesc& d, GemmPlan* p) {
 
 dflow_status plan_rows(dflow_session* s, int64_t rows) {
   if (rows == s->planned_rows) return DFLOW_OK;
-  const int max_ctas = (s->opt.world > 1 && s->opt.overlap && s->opt.sm_reserve > 0)
+  const int max_ctas = (s->replicas > 1 && s->opt.overlap && s->opt.sm_reserve > 0)
                            ? std::max(2, s->num_sms - s->opt.sm_reserve)
                            : 0;
   const bool tf = s->tf32;
@@ -486,6 +528,11 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       f.epilogue = EPI_BIAS_RELU;
       f.out = ly.A.hi; f.out2 = ly.A.lo; f.ldo = ly.ld_out;
       ST(gemm_plan(s, f, &ly.fwd));
+      if (s->mp && l + 1 == s->mp_hi) {  // f4: this activation crosses to rank+1 as its channel code
+        GemmDesc fs = f;
+        fs.trunc_out = 1;
+        ST(gemm_plan(s, fs, &ly.fwd_send));
+      }
     } else {
       // last layer: Relu + loss seed + db partials fused (a1 + a2 + a5); y is patched per call
       f.epilogue = EPI_BIAS_RELU_LOSS;
@@ -519,6 +566,13 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.max_ctas = max_ctas;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
+      if (s->mp && l == s->mp_lo) {  // f4: dA_{l-1} crosses back to rank-1 as channel codes (no mask here)
+        GemmDesc ds = d;
+        ds.epilogue = EPI_TRUNC16;
+        ds.mask = nullptr; ds.ldm = 0; ds.colsum_ws = nullptr;
+        ds.out = lp.dZ.hi; ds.out2 = nullptr; ds.ldo = lp.ld_out;
+        ST(gemm_plan(s, ds, &ly.dgrad_send));
+      }
     }
     GemmDesc w{};
     w.tf32 = tf;
@@ -529,7 +583,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     w.out_f32 = ly.g32; w.ldo32 = ly.out;
     w.max_ctas = max_ctas;
     ST(gemm_plan(s, w, &ly.wgrad32));
-    if (s->opt.world == 1 && s->trainable) {
+    if (s->replicas == 1 && s->trainable) {
       // no channel (reading A6): ApplyGradientDescent fused into the dW epilogue
       GemmDesc wa = w;
       wa.epilogue = EPI_SGD_APPLY;
@@ -552,7 +606,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       wa.sgd_lr = ly.n.lr_W;
       ST(gemm_plan(s, wa, &ly.wgrad_async));
     }
-    if (s->opt.world > 1 && u16_wire(s) && !s->p2p && !s->async) {
+    if (s->replicas > 1 && u16_wire(s) && !s->p2p && !s->async) {
       w.epilogue = EPI_TRUNC16;
       w.out_f32 = nullptr;
       w.out = ly.q16; w.out2 = nullptr; w.ldo = ly.out;
@@ -702,7 +756,7 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
 // Exchange + apply of layer l (comm stream when N > 1).
 dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
   Layer& ly = s->layers[l];
-  const int N = s->opt.world;
+  const int N = s->replicas;
   const int64_t nW = ly.in * ly.out;
   cudaStream_t cs = st;
   const uint16_t* g16 = nullptr;
@@ -788,7 +842,7 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     }
     return DFLOW_OK;
   }
-  const bool t16 = mode == 0 && s->opt.world > 1 && u16_wire(s);
+  const bool t16 = mode == 0 && s->replicas > 1 && u16_wire(s);
   for (int l = s->L - 1; l >= 0; --l) {
     Layer& ly = s->layers[l];
     if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
@@ -810,7 +864,90 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
     if (mode == 0) ST(exchange_apply(s, l, st));
   }
-  if (mode == 0 && s->opt.world > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
+  if (mode == 0 && s->replicas > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
+  return DFLOW_OK;
+}
+
+// ---------------------------------------------------------------- f4 model parallelism
+// Rank r runs layers [mp_lo, mp_hi) of one replica.  Channels (readings A32-A33) on `st`:
+// forward, the activation of layer mp_hi-1 (as truncation codes) to rank r+1; backward,
+// dA of layer mp_lo (codes) to rank r-1.  NCCL point-to-point moves the bytes.
+dflow_status run_forward_mp(dflow_session* s, const Feeds& f, int64_t rows, cudaStream_t st) {
+  const int R = s->opt.rank, N = s->opt.world, lo = s->mp_lo, hi = s->mp_hi;
+  if (lo == 0) {
+    if (!f.x) return fail(DFLOW_INVALID_ARGUMENT, "x must be fed");
+    const int t = tbegin(s, 1, st);
+    cudaError_t e = (s->x_dtype == DFLOW_F32)
+                        ? to_operand(s, static_cast<const float*>(f.x), f.ldx, s->A0, s->ld_A0, rows, s->layers[0].in, st)
+                        : launch_copy_bf16(static_cast<const __nv_bfloat16*>(f.x), f.ldx,
+                                           static_cast<__nv_bfloat16*>(s->A0.hi), s->ld_A0, rows, s->layers[0].in, st);
+    tend(s, t, st);
+    ST(check_launch(s, e, 1, "input cast"));
+  } else {
+    const Layer& lp = s->layers[lo - 1];  // the received codes are the bf16 operand bits
+    NC(ncclRecv(lp.A.hi, static_cast<size_t>(rows * lp.ld_out) * 2, ncclUint8, R - 1, s->nccl, st));
+  }
+  for (int l = lo; l < hi; ++l) {
+    Layer& ly = s->layers[l];
+    if (l + 1 < s->L) {
+      ST(launch_gemm(s, (l + 1 == hi) ? ly.fwd_send : ly.fwd, st));
+      continue;
+    }
+    // last layer (last rank): Relu + loss seed + db partials
+    const bool need_y = s->loss_kind == DFLOW_LOSS_MSE;
+    if (need_y && !f.y) return fail(DFLOW_INVALID_ARGUMENT, "y must be fed (MSE loss)");
+    if (need_y && f.ldy < ly.out) return fail(DFLOW_INVALID_ARGUMENT, "ld of y < its width");
+    ly.fwd.args.y = f.y;
+    ly.fwd.args.ldy = f.ldy;
+    if (s->y_upload_pending) {  // host-fed y
+      CU(cudaStreamWaitEvent(st, s->ev_h2d_y, 0));
+      s->y_upload_pending = false;
+    }
+    ST(launch_gemm(s, ly.fwd, st));
+    const int t = tbegin(s, 1, st);
+    cudaError_t e = launch_loss_final(need_y ? 0 : 1, s->loss_partials, ly.fwd.grid * 4, rows, ly.out, s->loss_dev, st);
+    tend(s, t, st);
+    ST(check_launch(s, e, 1, "loss reduction"));
+  }
+  if (R + 1 < N) {
+    const Layer& ll = s->layers[hi - 1];
+    NC(ncclSend(ll.A.hi, static_cast<size_t>(rows * ll.ld_out) * 2, ncclUint8, R + 1, s->nccl, st));
+  }
+  s->have_forward = true;
+  s->last_rows = rows;
+  return DFLOW_OK;
+}
+
+dflow_status run_backward_mp(dflow_session* s, int64_t rows, cudaStream_t st) {
+  const int R = s->opt.rank, N = s->opt.world, lo = s->mp_lo, hi = s->mp_hi;
+  for (int l = hi - 1; l >= lo; --l) {
+    Layer& ly = s->layers[l];
+    if (l == hi - 1 && R + 1 < N) {
+      // the received dA codes, masked by this rank's own activation (ReluGrad on the
+      // channel's output) -> dZ and its per-32-row column partials
+      NC(ncclRecv(s->mp_recv, static_cast<size_t>(rows * ly.ld_out) * 2, ncclUint8, R + 1, s->nccl, st));
+      const int t = tbegin(s, 1, st);
+      cudaError_t e = launch_relugrad_recv(s->mp_recv, ly.ld_out, static_cast<const __nv_bfloat16*>(ly.A.hi), ly.ld_out,
+                                           rows, ly.out, static_cast<__nv_bfloat16*>(ly.dZ.hi), ly.ld_out,
+                                           ly.colsum_ws, st);
+      tend(s, t, st);
+      ST(check_launch(s, e, 1, "channel ReluGrad"));
+    }
+    if (l > lo) {
+      ST(launch_gemm(s, ly.dgrad, st));
+    } else if (l > 0) {  // l == lo on rank > 0: dA_{lo-1} leaves as codes
+      ST(launch_gemm(s, ly.dgrad_send, st));
+      const Layer& lp = s->layers[l - 1];
+      NC(ncclSend(lp.dZ.hi, static_cast<size_t>(rows * lp.ld_out) * 2, ncclUint8, R - 1, s->nccl, st));
+    }
+    ST(launch_gemm(s, ly.wgrad_apply, st));  // this rank's own update (no replicas: reading A6)
+    const int t = tbegin(s, 1, st);
+    cudaError_t e = launch_colsum_final(ly.colsum_ws, static_cast<int>((rows + 31) / 32), ly.out,
+                                        ly.g32 + ly.in * ly.out, nullptr, st);
+    tend(s, t, st);
+    ST(check_launch(s, e, 1, "bias-gradient column sum"));
+    ST(exchange_apply(s, l, st));  // replicas == 1: the bias update
+  }
   return DFLOW_OK;
 }
 
@@ -839,7 +976,14 @@ cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st) {
 }
 
 dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
-  if (s->opt.world > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
+  if (s->mp) {  // f4: the last rank computed C; every rank reports it
+    NC(ncclBroadcast(s->loss_dev, s->loss_dev, 1, ncclFloat32, s->opt.world - 1, s->nccl, st));
+    CU(cudaMemcpyAsync(s->loss_host, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    CU(record_event(s, s->ev_loss_ready, st));
+    s->loss_pending = true;
+    return DFLOW_OK;
+  }
+  if (s->replicas > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
     CU(cudaEventRecord(s->ev_loss, st));
     CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
     NC(ncclAllReduce(s->loss_dev, s->loss_dev + 1, 1, ncclFloat32, ncclSum, s->nccl, s->comm));
@@ -858,7 +1002,7 @@ dflow_status wait_loss(dflow_session* s, float* loss_out) {
   s->loss_pending = false;
   CU(cudaEventSynchronize(s->ev_loss_ready));
   float v = s->loss_host[0];
-  if (s->opt.world > 1 && !s->async) v /= static_cast<float>(s->opt.world);
+  if (s->replicas > 1 && !s->async) v /= static_cast<float>(s->opt.world);
   if (loss_out) *loss_out = v;
   s->nonfinite = std::isfinite(v) ? 0 : 1;
   return DFLOW_OK;
@@ -892,6 +1036,12 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   s->cap = opt.max_local_rows;
   s->tf32 = opt.precision == DFLOW_PRECISION_3XTF32;
   s->esz = s->tf32 ? 4 : 2;
+  s->mp = opt.model_parallel != 0 && opt.world > 1;
+  s->replicas = s->mp ? 1 : opt.world;  // data-parallel replicas (model parallelism: one)
+  if (s->mp && (opt.async_dp || opt.precision != DFLOW_PRECISION_BF16)) {
+    delete s;
+    return fail(DFLOW_INVALID_ARGUMENT, "model_parallel runs the bf16 path without async_dp");
+  }
   s->async = opt.async_dp != 0 && opt.world > 1;
   if (s->async && (s->tf32 || !(opt.exchange == DFLOW_EXCHANGE_TRUNC16 || opt.exchange == DFLOW_EXCHANGE_SR16 ||
                                  opt.exchange == DFLOW_EXCHANGE_FP32))) {
@@ -902,11 +1052,12 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     delete s;
     return fail(DFLOW_INVALID_ARGUMENT, "async_dp supports up to %d ranks", kMaxRanks);
   }
-  s->p2p = !s->async && opt.p2p && opt.world > 1 &&
+  s->p2p = !s->async && !s->mp && opt.p2p && opt.world > 1 &&
            (opt.exchange == DFLOW_EXCHANGE_TRUNC16 || opt.exchange == DFLOW_EXCHANGE_SR16);
-  dflow_status st = insert_exchange(user, opt.world, opt.exchange | (s->async ? DFLOW_EXCHANGE_ASYNC : 0), &s->g,
+  dflow_status st = insert_exchange(user, s->replicas, opt.exchange | (s->async ? DFLOW_EXCHANGE_ASYNC : 0), &s->g,
                                     &s->remap);
   if (st == DFLOW_OK) st = match_graph(s);
+  if (st == DFLOW_OK && s->mp) st = setup_mp(s);
   if (st == DFLOW_OK && s->tf32 && s->x_dtype != DFLOW_F32)
     st = fail(DFLOW_INVALID_ARGUMENT, "the 3xTF32 path needs an fp32 x placeholder");
   if (st != DFLOW_OK) {
@@ -930,7 +1081,9 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     return fail(DFLOW_CUDA, "dflow kernels are built for sm_100a; device is sm_%d%d", prop.major, prop.minor);
   }
   s->num_sms = prop.multiProcessorCount;
-  st = alloc_state(s);
+  if (st == DFLOW_OK) st = alloc_state(s);
+  if (st == DFLOW_OK && s->mp && s->mp_hi < s->L)
+    st = dmalloc(s, &s->mp_recv, s->cap * s->layers[s->mp_hi - 1].ld_out);
   if (st == DFLOW_OK && opt.world > 1) {
     ncclUniqueId id;
     memcpy(&id, nccl_id, sizeof id);
@@ -965,6 +1118,7 @@ void session_destroy(dflow_session* s) {
     free_operand(ly.dZ);
   }
   free_operand(s->A0);
+  if (s->mp_recv) cudaFree(s->mp_recv);
   for (void* p : {(void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0],
                   s->host_stage[1], s->xbuf[0], s->xbuf[1], s->xbuf[2], s->xbuf[3]})
     if (p) cudaFree(p);
@@ -994,10 +1148,17 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   auto body = [&](cudaStream_t stream) -> dflow_status {
     s->launches = s->gemm_launches = 0;
     if (s->async && s->opt.async_dp == 1) ST(async_pull(s, stream));  // the replica reads the shared parameters
-    ST(run_forward(s, f, rows, stream, FWD_TRAIN));
-    CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
-    if (loss_out) ST(enqueue_loss(s, stream));
-    ST(run_backward(s, rows, stream, 0));
+    if (s->mp) {  // f4: this rank's layers of the one replica
+      ST(run_forward_mp(s, f, rows, stream));
+      CU(record_event(s, s->ev_feeds_free, stream));
+      ST(enqueue_loss(s, stream));  // every rank takes part in the loss broadcast
+      ST(run_backward_mp(s, rows, stream));
+    } else {
+      ST(run_forward(s, f, rows, stream, FWD_TRAIN));
+      CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
+      if (loss_out) ST(enqueue_loss(s, stream));
+      ST(run_backward(s, rows, stream, 0));
+    }
     s->last_launches = s->launches;
     s->last_gemm_launches = s->gemm_launches;
     return DFLOW_OK;
@@ -1095,6 +1256,7 @@ dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_
 
 dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
                              const int64_t* ld, int64_t rows, dflow_node fetch, void* out, cudaStream_t st) {
+  if (s->mp) return fail(DFLOW_UNIMPLEMENTED, "model_parallel sessions run train steps only");
   ST(check_rows(s, rows));
   Feeds f;
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
@@ -1127,6 +1289,7 @@ dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* fe
 dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                      const void* const* ptrs, const int64_t* ld, int64_t rows, int n,
                                      const dflow_node* grads, void* const* out, cudaStream_t st) {
+  if (s->mp) return fail(DFLOW_UNIMPLEMENTED, "model_parallel sessions run train steps only");
   if (s->lossgrad < 0) return fail(DFLOW_UNIMPLEMENTED, "graph has no gradient nodes");
   ST(check_rows(s, rows));
   Feeds f;

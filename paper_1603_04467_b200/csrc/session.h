@@ -52,6 +52,7 @@ struct Layer {
   P2PLayer p2p;                   // fused NVLink exchange: peer pointers of this layer
   AsyncLayer async;               // asynchronous replicas (f3): every rank's shard of this layer
   GemmPlan fwd, fwd_fetch, fwd_plain, dgrad, wgrad32, wgrad16, wgrad_apply, wgrad_p2p, wgrad_async;
+  GemmPlan fwd_send, dgrad_send;  // f4 channel ends: truncation-coded activation out / dA out
   bool has_fwd = false, has_dgrad = false, has_wgrad16 = false, has_wgrad_apply = false, has_wgrad_p2p = false;
 };
 
@@ -119,6 +120,11 @@ struct dflow_session {
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;
   bool async = false;  // opt.async_dp (f3): sym holds this rank's parameter shards
+  // opt.model_parallel (f4): this rank holds layers [mp_lo, mp_hi); channel buffers
+  bool mp = false;
+  int replicas = 1;    // data-parallel replicas (world, or 1 under model parallelism)
+  int mp_lo = 0, mp_hi = 0;
+  uint16_t* mp_recv = nullptr;  // codes of dA of layer mp_hi-1 from rank+1 [cap, ld_out]
   void* sym = nullptr;
   void* peer_sym[dflow::kMaxRanks] = {};
   int* p2p_done = nullptr;

@@ -183,3 +183,47 @@ def test_round16_key_matches_the_oracle_key_derivation():
                     for rank in (0, 5):
                         D.check(D.dflow_round16_key(seed, step, layer, stage, rank, C.byref(k)))
                         assert k.value == sr_key(seed, step, layer, stage, rank)
+
+
+@pytest.mark.parametrize("dims,world", [((16, 8, 4), 2), ((8, 6, 4, 2), 3), ((8, 8, 8, 8, 8), 2), ((8, 8, 8, 8, 8), 4)])
+def test_partition_pass_matches_oracle_partition(dims, world):
+    # f4: the C partition pass and the oracle's give the same per-device
+    # subgraphs (Send/Recv canonicalised per endpoint and destination, channel codec)
+    from oracle.partition import partition, place_mlp
+    mg = build_mlp(dims, "MSE", 0.5)
+    m = D.mlp_graph(dims, "MSE", 0.5)
+    try:
+        names = [n["name"] for n in json.loads(D.graph_json(m.graph))["nodes"]]
+        place = place_mlp(mg, world)
+        arr = (C.c_int32 * len(names))(*[place[nm] for nm in names])
+        ref = partition(mg.graph, place)
+        for d in range(world):
+            out = C.c_void_p()
+            D.check(D.dflow_graph_partition(m.graph, arr, len(names), d, 1, C.byref(out)))
+            try:
+                assert _canon(D.graph_json(out)) == _canon(ref[d].to_json()), d
+            finally:
+                D.dflow_graph_destroy(out)
+    finally:
+        D.dflow_graph_destroy(m.graph)
+
+
+@pytest.mark.parametrize("dims,world", [((16, 8, 4), 2), ((8, 8, 8, 8, 8), 4)])
+def test_model_parallel_session_plans(dims, world):
+    # f4: the planner + partition check accept the layer-partitioned MLP (on CPU the session
+    # stops at the missing device, never at UNIMPLEMENTED); more ranks than layers is refused
+    m = D.mlp_graph(dims, "MSE", 0.5)
+    try:
+        for rank in range(world):
+            opts = D.make_options(world=world, rank=rank, max_local_rows=8, model_parallel=1)
+            s = C.c_void_p()
+            st = D.dflow_session_create(m.graph, C.byref(opts), (C.c_uint8 * 128)(), C.byref(s))
+            assert st in (D.DFLOW_OK, D.DFLOW_CUDA), D.dflow_last_error()
+            if st == D.DFLOW_OK:
+                D.dflow_session_destroy(s)
+        opts = D.make_options(world=len(dims), rank=0, max_local_rows=8, model_parallel=1)
+        s = C.c_void_p()
+        assert D.dflow_session_create(m.graph, C.byref(opts), (C.c_uint8 * 128)(), C.byref(s)) == \
+            D.DFLOW_INVALID_ARGUMENT
+    finally:
+        D.dflow_graph_destroy(m.graph)
