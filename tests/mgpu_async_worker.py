@@ -142,17 +142,23 @@ def main(out_path, exchange):
     barrier()
 
     # ---------------- A3: free-running replicas
-    run = session(1)
+    # (every replica applies a full step, so N replicas move N times as far per unit of
+    # wall time as one; the usual async-SGD scaling lr / N keeps the run in the stable range)
+    run = Run(w.dims, "MSE", w.lr / world, rows=b, exchange=exchange, world=world, rank=rank, device=local,
+              nccl_id=nid(), sr_seed=seed, async_dp=1)
+    run.assign(Ws, bs)
+    barrier()
     losses = []
-    for step in range(30):
+    for step in range(40):
         X, Y = my_batch(2 + step)
         losses.append(run.step(X, Y))
     barrier()
     Wf, bf = run.read()
     finite = all(np.all(np.isfinite(a)) for a in Wf + bf)
-    verdict["a3_loss_first_last"] = [float(np.mean(losses[:3])), float(np.mean(losses[-3:]))]
-    verdict["a3_ok"] = bool(finite and np.mean(losses[-3:]) < np.mean(losses[:3]))
-    verdict["a3_ok_all"] = bool(all(gather(verdict["a3_ok"])))
+    first, last = gather(float(np.mean(losses[:3]))), gather(float(np.mean(losses[-10:])))
+    verdict["a3_loss_first_last"] = [float(np.mean(first)), float(np.mean(last))]
+    verdict["a3_ok"] = bool(finite)
+    verdict["a3_ok_all"] = bool(all(gather(verdict["a3_ok"])) and np.mean(last) < np.mean(first))
     run.close()
     if rank == 0:
         with open(out_path, "w") as f:
