@@ -149,6 +149,27 @@ def oracle_sample(w: synth.Workload, target_s: float, n_steps: int = 1):
     return rows, times
 
 
+def numpy_f32_sample(w: synth.Workload, rows: int):
+    """The best plain-CPU line: the same step in numpy float32 (multithreaded
+    BLAS), no graph, no codec — forward, MSE seed, backward, SGD — on a row sample."""
+    import numpy as np
+    Ws, bs = synth.init_params(w)
+    X, Y = synth.batch(w, rows=rows)
+    t0 = time.perf_counter()
+    acts = [X]
+    for W, b in zip(Ws, bs):
+        acts.append(np.maximum(acts[-1] @ W + b, np.float32(0)))
+    g = (acts[-1] - Y) / np.float32(rows * w.dims[-1])
+    for l in range(len(Ws) - 1, -1, -1):
+        g = g * (acts[l + 1] > 0)
+        dW, db = acts[l].T @ g, g.sum(0)
+        if l:
+            g = g @ Ws[l].T
+        Ws[l] -= np.float32(w.lr) * dW
+        bs[l] -= np.float32(w.lr) * db
+    return time.perf_counter() - t0
+
+
 def cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -259,16 +280,21 @@ def run_gpu(args, w):
     for _ in range(max(0, args.warmup - 1)):
         step()
     clocks = Clocks(local)
-    barrier()
     clocks.start()
+    # the median of `repeats` timed regions of exactly K steps each, every one
+    # bracketed by barrier + synchronize, max over ranks
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    barrier()
+    ms_list = []
+    for _ in range(max(1, args.repeats)):
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+        ms_list.append(max_over_ranks(e0.elapsed_time(e1), dist, "cuda"))
     clk = clocks.stop()
-    ms = max_over_ranks(e0.elapsed_time(e1), dist, "cuda")
+    ms = sorted(ms_list)[len(ms_list) // 2]
     st = D.dflow_stats()
     D.check(D.dflow_session_stats(s, C.byref(st)))
     launches = st.launches_per_step
@@ -327,9 +353,14 @@ def run_gpu(args, w):
             cpu = {"value": rows / times[0], "unit": UNIT, "cores": cores(), "kind": "oracle",
                    "sample": f"one oracle (f64 numpy graph executor) train step of {w.name} on a {rows}-row "
                              f"sample of the global batch ({times[0]:.1f} s)"}
+            f32_rows = max(256, min(w.batch, rows * 8))
+            t32 = numpy_f32_sample(w, f32_rows)
+            cpu32 = {"value": f32_rows / t32, "unit": UNIT, "cores": cores(), "kind": "numpy_f32",
+                     "sample": f"one plain numpy float32 step (BLAS) of {w.name} on {f32_rows} rows ({t32:.1f} s)"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "repeats": len(ms_list), "ms_per_step_repeats": [m / args.steps for m in ms_list],
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 (3xTF32)" if tf32 else "bf16",
             "data": "synthetic (seeded, synth/; X,Y ~ U[0,1), He-uniform W)",
             "config": config_dict(w, args, world),
@@ -348,6 +379,7 @@ def run_gpu(args, w):
                          "avg_launch_ms": gemm_avg_ms, "flops_per_launch": flops_per_launch,
                          "gemm_share_of_step": st.gemm_ms / max(1e-9, st.gemm_ms + st.other_ms + st.exchange_ms)},
             "cpu_baseline": cpu,
+            "cpu_f32": cpu32 if (world == 1 and not args.no_cpu_baseline) else None,
             "e2e": {"value": w.batch * e2e_steps / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(X.nbytes + Y.nbytes) * world, "d2h_bytes_per_step": 4 * world},
             "gpu_launches": launches * args.steps,
@@ -372,6 +404,8 @@ def main():
     ap.add_argument("--config", default="C3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="override the global batch (parity/debug only)")
     ap.add_argument("--exchange", default="TRUNC16", choices=["TRUNC16", "FP32", "FP32_NCCL", "NONE", "SR16"])
+    ap.add_argument("--repeats", type=int, default=3,
+                    help="timed regions of K steps each; value = the median (SURVEY §8(d))")
     ap.add_argument("--model-parallel", type=int, default=0,
                     help="N > 1: 1 = layer-wise model parallelism (f4): rank r holds layers "
                          "[r L / N, (r+1) L / N), activations / their gradients cross through Send/Recv "
