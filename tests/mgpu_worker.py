@@ -31,6 +31,9 @@ import synth  # noqa: E402
 
 def main(out_path, exchange):
     p2p = 0
+    precision = "bf16"
+    if exchange.endswith("_TF32"):  # the fp32-faithful 3xTF32 path over the same channel
+        exchange, precision = exchange[:-5], "3xtf32"
     if exchange.endswith("_P2P"):  # the fused NVLink exchange (f1): same bits as the NCCL path
         exchange, p2p = exchange[:-4], 1
     seed = 1234  # SR16 draw streams (reading A27)
@@ -51,7 +54,8 @@ def main(out_path, exchange):
     X, Y = synth.batch(w)
     Xr, Yr = X[rank * b:(rank + 1) * b], Y[rank * b:(rank + 1) * b]
     run = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local, nccl_id=nid,
-              p2p=p2p, sr_seed=seed)
+              p2p=p2p, sr_seed=seed, precision=precision)
+    verdict["precision"] = precision
     run.assign(Ws, bs)
     Xd, Yd = torch.from_numpy(Xr).cuda(), torch.from_numpy(Yr).cuda()
 

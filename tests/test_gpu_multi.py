@@ -35,7 +35,8 @@ def _run(n, exchange, tmp_path):
     return json.load(open(out))
 
 
-@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL", "SR16", "SR16_P2P"])
+@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL", "SR16", "SR16_P2P",
+                                      "TRUNC16_P2P_TF32", "FP32_TF32"])
 def test_two_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 2:
@@ -46,7 +47,10 @@ def test_two_gpu_replicated_step(exchange, tmp_path):
     assert v["p11_replicas_identical"] and v["p11_after_4_steps"], v
     if exchange != "FP32_NCCL":
         assert v["p4_step_bitexact"], v
-    assert v["w_after_max_err"] < 2e-2, v
+    # bf16: the north-star 2e-2; 3xTF32 with the FP32 channel: 1e-4; 3xTF32 with TRUNC16: the
+    # codec's two truncations (2^-7 each) dominate, so the bf16-level gate applies
+    tol = 1e-4 if exchange == "FP32_TF32" else 2e-2
+    assert v["w_after_max_err"] < tol, v
 
 
 @pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "SR16_P2P"])
