@@ -457,7 +457,10 @@ __global__ void __launch_bounds__(256, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (CG == 2) ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+          // relaxed: the reads it releases completed at tcgen05.wait::ld; a release.cluster
+          // arrive would add a GPU-scope MEMBAR per TMEM hand-back (per 128-deep K chunk on
+          // the 3xTF32 path)
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
           else ptx::mbar_arrive(ptx::smem_u32(&tempty[acc]));
         }
         acc ^= 1;
