@@ -227,3 +227,22 @@ def test_model_parallel_session_plans(dims, world):
             D.DFLOW_INVALID_ARGUMENT
     finally:
         D.dflow_graph_destroy(m.graph)
+
+
+def test_option_validation_for_the_widening_rows():
+    # f3 / f4 option combinations the session refuses before touching a device
+    m = D.mlp_graph((16, 8, 4), "MSE", 0.5)
+    try:
+        bad = [dict(world=2, async_dp=1, precision=D.DFLOW_PRECISION_3XTF32),   # async: bf16 only
+               dict(world=2, async_dp=1, exchange="FP32_NCCL"),                  # async: TRUNC16/SR16/FP32
+               dict(world=2, model_parallel=1, async_dp=1),                     # one or the other
+               dict(world=2, model_parallel=1, precision=D.DFLOW_PRECISION_3XTF32),
+               dict(world=3, model_parallel=1),                                 # more ranks than layers
+               dict(world=2, exchange=9)]                                       # unknown exchange
+        for kw in bad:
+            opts = D.make_options(rank=0, max_local_rows=8, **kw)
+            s = C.c_void_p()
+            st = D.dflow_session_create(m.graph, C.byref(opts), (C.c_uint8 * 128)(), C.byref(s))
+            assert st == D.DFLOW_INVALID_ARGUMENT, (kw, st, D.dflow_last_error())
+    finally:
+        D.dflow_graph_destroy(m.graph)
