@@ -377,7 +377,12 @@ def run_gpu(args, w):
                          "frac_of_burst": achieved / peak_b, "peak_burst": peak_b,
                          "traffic": traffic, "peak_source": pk["source"] + peak_note,
                          "avg_launch_ms": gemm_avg_ms, "flops_per_launch": flops_per_launch,
-                         "gemm_share_of_step": st.gemm_ms / max(1e-9, st.gemm_ms + st.other_ms + st.exchange_ms)},
+                         "gemm_share_of_step": st.gemm_ms / max(1e-9, st.gemm_ms + st.other_ms + st.exchange_ms),
+                         # device time per step by kind (CUDA events around every launch, rank 0;
+                         # exchange kernels run on the comm stream, overlapping the backward)
+                         "kernel_ms_per_step": {"gemm": st.gemm_ms / max(1, st.timed_steps),
+                                                "other": st.other_ms / max(1, st.timed_steps),
+                                                "exchange": st.exchange_ms / max(1, st.timed_steps)}},
             "cpu_baseline": cpu,
             "cpu_f32": cpu32 if (world == 1 and not args.no_cpu_baseline) else None,
             "e2e": {"value": w.batch * e2e_steps / e2e_s, "unit": UNIT,

@@ -1,6 +1,7 @@
 // Fused NVLink gradient exchange kernels (see exchange_p2p.h).  Arithmetic is the
 // same as the NCCL path (k_owner_reduce_t16): rank-order fp32 fold of the
 // expanded values, x (1/N), truncate — so both paths give the same bits.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -103,11 +104,68 @@ __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16
       const uint32_t hi = round16(__float_as_uint(__fmul_rn(s[e + 1], inv)), idx0 + e + 1, r16);
       o[e >> 1] = lo | (hi << 16);
     }
-    const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
-    for (int j = 0; j < p.world; ++j)  // all-gather leg: push q_bar to every rank (NVLink stores)
-      reinterpret_cast<uint4*>(p.gath[j] + static_cast<int64_t>(p.rank) * p.shard)[i] = ov;
+    if (!p.owner_apply) {
+      const uint4 ov = make_uint4(o[0], o[1], o[2], o[3]);
+      for (int j = 0; j < p.world; ++j)  // all-gather leg: push q_bar to every rank (NVLink stores)
+        reinterpret_cast<uint4*>(p.gath[j] + static_cast<int64_t>(p.rank) * p.shard)[i] = ov;
+      continue;
+    }
+    // owner-apply (a9 on the owner): W <- fl(W - fl(lr * g_hat)) on this rank's fp32 shard,
+    // then the new bf16 operand values / fp32 biases go to every rank (the gather leg)
+    const int64_t nw = p.in * p.out, nb = nw + p.out;
+    float gh[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) gh[e] = __uint_as_float(((o[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu) << 16);
+    if (idx0 + 8 <= nw && (p.out % 8) == 0) {
+      // 8 consecutive weights of one row: two float4 of the fp32 shard, one 16-byte bf16 store
+      // per rank (coalesced NVLink writes)
+      float4* w4 = reinterpret_cast<float4*>(p.w32[p.rank] + idx0);
+      float4 a = w4[0], b = w4[1];
+      float wn[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t h[4];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) wn[e] = __fsub_rn(wn[e], __fmul_rn(p.lr_w, gh[e]));
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        const __nv_bfloat162 v = __floats2bfloat162_rn(wn[e], wn[e + 1]);  // operand copy (reading A13)
+        h[e >> 1] = *reinterpret_cast<const uint32_t*>(&v);
+      }
+      w4[0] = make_float4(wn[0], wn[1], wn[2], wn[3]);
+      w4[1] = make_float4(wn[4], wn[5], wn[6], wn[7]);
+      const int64_t row = idx0 / p.out, col = idx0 - row * p.out;
+      const uint4 hv = make_uint4(h[0], h[1], h[2], h[3]);
+      for (int j = 0; j < p.world; ++j) *reinterpret_cast<uint4*>(p.wop[j] + row * p.ldwb + col) = hv;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int64_t idx = idx0 + e;
+        if (idx >= nb) break;  // bucket padding
+        if (idx < nw) {
+          float* w = p.w32[p.rank] + idx;
+          const float wn = __fsub_rn(*w, __fmul_rn(p.lr_w, gh[e]));
+          *w = wn;
+          const int64_t row = idx / p.out, col = idx - row * p.out;
+          const __nv_bfloat16 hh = __float2bfloat16_rn(wn);
+          const uint16_t hb = *reinterpret_cast<const uint16_t*>(&hh);
+          for (int j = 0; j < p.world; ++j) p.wop[j][row * p.ldwb + col] = hb;
+        } else {
+          const int64_t c = idx - nw;
+          const float bn = __fsub_rn(p.b32[p.rank][c], __fmul_rn(p.lr_b, gh[e]));
+          for (int j = 0; j < p.world; ++j) p.b32[j][c] = bn;
+        }
+      }
+    }
   }
   grid_signal(p, 1, epoch);
+}
+
+__global__ void k_gather_w32(const P2PLayer p) {
+  const int64_t nw = p.in * p.out;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nw; i += stride) {
+    const int owner = static_cast<int>(i / p.shard);
+    if (owner != p.rank) p.w32[p.rank][i] = __ldcv(p.w32[owner] + i);
+  }
 }
 
 __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
@@ -128,6 +186,13 @@ cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStrea
   const int64_t nv = p.shard / 8;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((nv + 255) / 256, 148 * 2)));
   k_owner_reduce_p2p<<<blocks, 256, 0, s>>>(p, epoch, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_w32(const P2PLayer& p, cudaStream_t s) {
+  const int64_t n = p.in * p.out;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8)));
+  k_gather_w32<<<blocks, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

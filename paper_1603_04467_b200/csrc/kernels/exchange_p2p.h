@@ -28,6 +28,14 @@ struct P2PLayer {
   int* done;                   // local grid-completion counters       [2]
   int64_t shard;
   int rank, world;
+  // owner-apply (SURVEY §8(e), bf16 path): the owner applies the update to its fp32 shard and
+  // pushes the new bf16 operand values (and fp32 biases) into every rank's copies
+  int owner_apply;
+  float* w32[kMaxRanks];       // rank j's fp32 master W [in*out] (dense, bucket order)
+  float* b32[kMaxRanks];       // rank j's fp32 bias [out]
+  uint16_t* wop[kMaxRanks];    // rank j's bf16 operand copy of W [in, ldwb]
+  int64_t in, out, ldwb;
+  float lr_w, lr_b;
 };
 
 // db_l (sum of the per-32-row partials), coded (truncate / SR16) and stored at bucket index
@@ -35,7 +43,11 @@ struct P2PLayer {
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
                                     uint32_t epoch, cudaStream_t s, Round16 r = {0, 0});
 // Owner step over peer memory (see above); the mean is coded with r (truncate or SR16).
+// With p.owner_apply the owner instead applies W <- fl(W - fl(lr * expand(q_bar))) to its own
+// shard and pushes bf16(W) / fp32 b to every rank (phase-1 flags then mean "parameters in").
 cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s, Round16 r = {0, 0});
+// owner-apply: this rank's fp32 W <- every owner's shard (NVLink loads), for reads of W
+cudaError_t launch_gather_w32(const P2PLayer& p, cudaStream_t s);
 // Block until all `world` phase-1 flags of this rank reach `epoch` (one CTA, acquire.sys).
 cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
 

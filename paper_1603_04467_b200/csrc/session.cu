@@ -448,6 +448,46 @@ dflow_status setup_p2p(dflow_session* s) {
     ly.p2p.rank = R;
     ly.p2p.world = N;
   }
+  if (s->tf32) return DFLOW_OK;
+  // owner-apply: every rank maps every peer's W32, b32 and bf16 W copy
+  const int per = 3 * s->L;  // handles per rank
+  std::vector<cudaIpcMemHandle_t> mine(per);
+  for (int l = 0; l < s->L; ++l) {
+    CU(cudaIpcGetMemHandle(&mine[3 * l], s->layers[l].W32));
+    CU(cudaIpcGetMemHandle(&mine[3 * l + 1], s->layers[l].b32));
+    CU(cudaIpcGetMemHandle(&mine[3 * l + 2], s->layers[l].Wop.hi));
+  }
+  uint8_t* hd = nullptr;
+  CU(cudaMalloc(&hd, 64 * per * (N + 1)));
+  CU(cudaMemcpy(hd, mine.data(), 64 * per, cudaMemcpyHostToDevice));
+  NC(ncclAllGather(hd, hd + 64 * per, 64 * per, ncclUint8, s->nccl, s->comm));
+  CU(cudaStreamSynchronize(s->comm));
+  std::vector<cudaIpcMemHandle_t> allh(per * N);
+  CU(cudaMemcpy(allh.data(), hd + 64 * per, 64 * per * N, cudaMemcpyDeviceToHost));
+  cudaFree(hd);
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    for (int j = 0; j < N; ++j) {
+      void* ptrs[3];
+      for (int k = 0; k < 3; ++k) {
+        if (j == R) {
+          ptrs[k] = k == 0 ? static_cast<void*>(ly.W32) : k == 1 ? static_cast<void*>(ly.b32) : ly.Wop.hi;
+        } else {
+          CU(cudaIpcOpenMemHandle(&ptrs[k], allh[j * per + 3 * l + k], cudaIpcMemLazyEnablePeerAccess));
+          s->peer_maps.push_back(ptrs[k]);
+        }
+      }
+      ly.p2p.w32[j] = static_cast<float*>(ptrs[0]);
+      ly.p2p.b32[j] = static_cast<float*>(ptrs[1]);
+      ly.p2p.wop[j] = static_cast<uint16_t*>(ptrs[2]);
+    }
+    ly.p2p.owner_apply = 1;
+    ly.p2p.in = ly.in;
+    ly.p2p.out = ly.out;
+    ly.p2p.ldwb = ly.ld_wb;
+    ly.p2p.lr_w = ly.n.lr_W;
+    ly.p2p.lr_b = ly.n.lr_b;
+  }
   return DFLOW_OK;
 }
 
@@ -640,7 +680,8 @@ int tbegin(dflow_session* s, int kind, cudaStream_t st) {
       s->event_pool.push_back(e);
     }
   }
-  TimedRange r{kind, s->event_pool[s->event_next], s->event_pool[s->event_next + 1]};
+  TimedRange r{kind, s->event_pool[s->event_next], s->event_pool[s->event_next + 1], st == s->comm ? 1 : 0,
+               nullptr};
   s->event_next += 2;
   cudaEventRecord(r.a, st);
   s->ranges.push_back(r);
@@ -653,6 +694,9 @@ void tend(dflow_session* s, int idx, cudaStream_t st) {
 
 dflow_status launch_gemm(dflow_session* s, const GemmPlan& p, cudaStream_t st) {
   const int t = tbegin(s, 0, st);
+  static const char* kEpi[] = {"F32", "TRUNC16", "BIAS_RELU", "RELUGRAD", "BIAS_RELU_LOSS", "SGD_APPLY",
+                               "TRUNC16_P2P", "ASYNC_PUSH"};
+  if (t >= 0 && p.d.epilogue >= 0 && p.d.epilogue < 8) s->ranges[t].label = kEpi[p.d.epilogue];
   cudaError_t e = gemm_launch(p, st);
   tend(s, t, st);
   if (e != cudaSuccess) {
@@ -776,6 +820,11 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
           ST(check_launch(s, launch_owner_reduce_p2p(ly.p2p, s->epoch, cs, own_code), 1, "owner reduce (p2p)"));
           ST(check_launch(s, launch_wait_flags(ly.p2p.flags[s->opt.rank] + kMaxRanks, N, s->epoch, cs), 1,
                           "gather wait (p2p)"));
+          if (ly.p2p.owner_apply) {  // the owners already updated W, b here (a9 on the owner)
+            tend(s, t, cs);
+            CU(cudaEventRecord(s->ev_apply[l], cs));
+            return DFLOW_OK;
+          }
           g16 = ly.p2p.gath[s->opt.rank];
           g32 = nullptr;
           break;
@@ -955,6 +1004,26 @@ dflow_status finish_timing(dflow_session* s, cudaStream_t st) {
   if (!s->timing) return DFLOW_OK;
   CU(cudaStreamSynchronize(st));
   if (s->comm) CU(cudaStreamSynchronize(s->comm));
+  // DFLOW_TIMELINE=<prefix>: the last timed step's launches as <prefix>.rank<R>.json
+  // (start / end in ms from the step's first launch, stream, kind, GEMM epilogue)
+  if (const char* tl = getenv("DFLOW_TIMELINE")) {
+    if (!s->ranges.empty()) {
+      std::string path = std::string(tl) + ".rank" + std::to_string(s->opt.rank) + ".json";
+      if (FILE* f = fopen(path.c_str(), "w")) {
+        fprintf(f, "[");
+        for (size_t i = 0; i < s->ranges.size(); ++i) {
+          const TimedRange& r = s->ranges[i];
+          float t0 = 0, t1 = 0;
+          cudaEventElapsedTime(&t0, s->ranges[0].a, r.a);
+          cudaEventElapsedTime(&t1, s->ranges[0].a, r.b);
+          fprintf(f, "%s{\"kind\": %d, \"comm\": %d, \"label\": \"%s\", \"t0\": %.4f, \"t1\": %.4f}",
+                  i ? ", " : "", r.kind, r.comm, r.label ? r.label : "", t0, t1);
+        }
+        fprintf(f, "]\n");
+        fclose(f);
+      }
+    }
+  }
   for (const TimedRange& r : s->ranges) {
     float ms = 0;
     cudaEventElapsedTime(&ms, r.a, r.b);
@@ -1106,6 +1175,7 @@ void session_destroy(dflow_session* s) {
   cudaDeviceSynchronize();
   for (int j = 0; j < dflow::kMaxRanks; ++j)
     if (s->peer_sym[j] && s->peer_sym[j] != s->sym) cudaIpcCloseMemHandle(s->peer_sym[j]);
+  for (void* p : s->peer_maps) cudaIpcCloseMemHandle(p);
   if (s->sym) cudaFree(s->sym);
   if (s->p2p_done) cudaFree(s->p2p_done);
   if (s->nccl) ncclCommDestroy(s->nccl);
@@ -1388,6 +1458,8 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
   cudaSetDevice(s->opt.device);
   Layer& ly = s->layers[l];
   if (s->async) ST(async_pull(s, st));  // the shared parameters, not this replica's last pull
+  if (s->p2p && ly.p2p.owner_apply && !is_bias)  // owner-apply: other shards live with their owners
+    CU(launch_gather_w32(ly.p2p, st));
   const float* src = is_bias ? ly.b32 : ly.W32;
   const size_t bytes = (is_bias ? ly.out : ly.in * ly.out) * sizeof(float);
   if (on_dev) {

@@ -59,6 +59,8 @@ struct Layer {
 struct TimedRange {
   int kind;  // 0 gemm, 1 other, 2 exchange
   cudaEvent_t a, b;
+  int comm;           // 1: launched on the comm stream
+  const char* label;  // GEMM epilogue name (timeline dump)
 };
 
 }  // namespace dflow
@@ -127,6 +129,7 @@ struct dflow_session {
   uint16_t* mp_recv = nullptr;  // codes of dA of layer mp_hi-1 from rank+1 [cap, ld_out]
   void* sym = nullptr;
   void* peer_sym[dflow::kMaxRanks] = {};
+  std::vector<void*> peer_maps;  // owner-apply: peers' W32 / b32 / W operand copies (CUDA IPC)
   int* p2p_done = nullptr;
   uint32_t epoch = 0;
   bool poisoned = false;
