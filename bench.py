@@ -132,13 +132,22 @@ def oracle_sample(w: synth.Workload, target_s: float, n_steps: int = 1):
     from oracle.mlp import build_mlp, train_step
     Ws, bs = synth.init_params(w)
     mg = build_mlp(w.dims, w.loss, w.lr)
-    rows = 16
-    X, Y = synth.batch(w, rows=rows)
-    t0 = time.perf_counter()
-    train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
-    t_probe = time.perf_counter() - t0
-    per_row = t_probe / rows
-    rows = int(max(16, min(w.batch, target_s / max(per_row, 1e-9))))
+    # a step costs fixed + per_row * rows, and the fixed part (the f64 update of every
+    # parameter, the graph walk) dominates small samples: double the rows until one step
+    # takes at least half the target, then size the sample from the last two probes
+    rows, probe = 32, []
+    while True:
+        X, Y = synth.batch(w, rows=rows)
+        t0 = time.perf_counter()
+        train_step(mg, Ws, bs, X, Y, 1, "TRUNC16")
+        probe.append((rows, time.perf_counter() - t0))
+        if probe[-1][1] >= 0.5 * target_s or rows >= w.batch:
+            break
+        rows = min(w.batch, rows * 2)
+    if len(probe) >= 2:
+        (r0, t0_), (r1, t1_) = probe[-2], probe[-1]
+        per_row = max((t1_ - t0_) / (r1 - r0), t1_ / r1 * 0.25, 1e-9)
+        rows = int(min(w.batch, r1 + max(0.0, target_s - t1_) / per_row))
     rows = max(16, rows // 16 * 16)
     X, Y = synth.batch(w, rows=rows)
     times = []
