@@ -224,6 +224,8 @@ def config_dict(w, args, world):
                          ("_P2P" if (args.exchange in ("TRUNC16", "SR16") and world > 1 and getattr(args, "p2p", 0)
                                      and not getattr(args, "async_dp", 0)) else "")),
             "parallelism": (f"mp{world}" if (world > 1 and getattr(args, "model_parallel", 0)) else f"dp{world}"),
+            "defer_apply": int(bool(world > 1 and getattr(args, "defer_apply", 0) and
+                                    not getattr(args, "model_parallel", 0) and not getattr(args, "async_dp", 0))),
             "precision": ("3xTF32 split fp32 operands (big, small), fp32 accumulate + master weights"
                           if w.precision == "3xtf32" else "bf16 operands, fp32 accumulate + master weights"),
             "l2": ("no flush: every step streams inputs and activations far larger than the 126 MB L2 "
@@ -258,6 +260,7 @@ def run_gpu(args, w):
                           overlap=1, sm_reserve=args.sm_reserve, p2p=args.p2p, sr_seed=1234,
                           graphs=1 if world == 1 else 0, async_dp=args.async_dp if world > 1 else 0,
                           model_parallel=1 if mp else 0,
+                          defer_apply=args.defer_apply if (world > 1 and not mp and not args.async_dp) else 0,
                           precision=D.DFLOW_PRECISION_3XTF32 if tf32 else D.DFLOW_PRECISION_BF16)
     s = D.session_create(mlp, opts, nid)
     Ws, bs = synth.init_params(w)
@@ -427,6 +430,9 @@ def main():
     ap.add_argument("--async-dp", type=int, default=0,
                     help="N > 1: 1 = asynchronous replicas (f3): each rank pulls the shared parameters, steps "
                          "and pushes its own coded update with no barrier (the exchange names the coding)")
+    ap.add_argument("--defer-apply", type=int, default=0,
+                    help="N > 1 synchronous: last two dW swapped, layer l's update joined only by the next "
+                         "forward of layer l (options.defer_apply; same bits)")
     ap.add_argument("--sm-reserve", type=int, default=0)
     ap.add_argument("--p2p", type=int, default=1,
                     help="TRUNC16 at N > 1: 1 = fused NVLink exchange (dW epilogue stores into the owners' "

@@ -168,6 +168,15 @@ typedef struct {
                              signature (x, y pointers, leading dims, rows) and replay it — one
                              launch per step instead of ~4L host launches (latency-bound C2);
                              the captured kernels and their arguments are the same             */
+  int32_t defer_apply;    /* synchronous world > 1 (not async_dp / model_parallel): 1 = the backward
+                             runs layers L..1 with the last two dW swapped (..., dgrad 2, dW 1,
+                             dW 2) and the step does not join the exchange stream: the update of
+                             layer l is waited for right before the next forward of layer l, so
+                             the last exchange (layer 2) overlaps the next step's layer 1 instead
+                             of ending the step.  Every later dflow
+                             call on any stream is ordered after the pending updates; a plain
+                             synchronize of `stream` alone is not (dflow_session_sync joins them).
+                             Same arithmetic, same bits as 0                                   */
 } dflow_options;
 
 /* 128-byte NCCL unique id for rank 0 to broadcast (e.g. via torch.distributed). */
@@ -234,6 +243,9 @@ typedef struct {
   int64_t timed_steps;
   double gemm_flops_per_step; /* algorithmic GEMM FLOPs of one step on this rank    */
 } dflow_stats;
+/* Orders `stream` after every update still pending on the session's exchange stream
+ * (options.defer_apply); a no-op otherwise.                                     */
+dflow_status dflow_session_sync(dflow_session* s, void* stream);
 /* Per-kernel CUDA-event timing inside dflow_train_step (off by default). */
 dflow_status dflow_session_set_timing(dflow_session* s, int enable);
 dflow_status dflow_session_stats(dflow_session* s, dflow_stats* out);

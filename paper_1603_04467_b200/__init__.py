@@ -44,7 +44,8 @@ class dflow_options(C.Structure):
     _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32), ("precision", C.c_int32),
                 ("exchange", C.c_int32), ("overlap", C.c_int32), ("sm_reserve", C.c_int32),
                 ("max_local_rows", C.c_int64), ("p2p", C.c_int32), ("sr_seed", C.c_uint32),
-                ("async_dp", C.c_int32), ("model_parallel", C.c_int32), ("graphs", C.c_int32)]
+                ("async_dp", C.c_int32), ("model_parallel", C.c_int32), ("graphs", C.c_int32),
+                ("defer_apply", C.c_int32)]
 
 
 class dflow_stats(C.Structure):
@@ -89,6 +90,7 @@ _SIGS = {
     "dflow_fetch_gradients": (_i32, [_p, _i32, _pnode, C.POINTER(_p), _pi64, _i64, _i32, _pnode, C.POINTER(_p), _p]),
     "dflow_fetch_relu_masks": (_i32, [_p, _i32, C.POINTER(C.c_uint32)]),
     "dflow_session_set_timing": (_i32, [_p, _i32]),
+    "dflow_session_sync": (_i32, [_p, _p]),
     "dflow_session_stats": (_i32, [_p, C.POINTER(dflow_stats)]),
     "dflow_truncate16": (_i32, [_p, _p, _sz, _p]),
     "dflow_round16": (_i32, [_p, _p, _sz, C.c_uint32, C.c_int, C.c_int64, _p]),
@@ -223,10 +225,10 @@ def _node_name(g, nid) -> bytes:
 
 def make_options(world=1, rank=0, device=0, precision=DFLOW_PRECISION_BF16, exchange="TRUNC16", overlap=1,
                  sm_reserve=0, max_local_rows=1, p2p=0, sr_seed=0, graphs=0, async_dp=0,
-                 model_parallel=0) -> dflow_options:
+                 model_parallel=0, defer_apply=0) -> dflow_options:
     ex = EXCHANGES[exchange] if isinstance(exchange, str) else int(exchange)
     return dflow_options(world, rank, device, precision, ex, overlap, sm_reserve, max_local_rows, p2p, sr_seed,
-                         async_dp, model_parallel, graphs)
+                         async_dp, model_parallel, graphs, defer_apply)
 
 
 def session_create(mlp_or_graph, opts: dflow_options, nccl_id: bytes = None):

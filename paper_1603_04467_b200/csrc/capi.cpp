@@ -317,6 +317,13 @@ dflow_status dflow_session_set_timing(dflow_session* s, int enable) {
   return DFLOW_OK;
 }
 
+dflow_status dflow_session_sync(dflow_session* s, void* stream) {
+  GUARD_BEGIN
+  if (!s) return fail(DFLOW_INVALID_ARGUMENT, "session is NULL");
+  return dflow::session_sync(s, static_cast<cudaStream_t>(stream));
+  GUARD_END
+}
+
 dflow_status dflow_session_stats(dflow_session* s, dflow_stats* out) {
   if (!s) return fail(DFLOW_INVALID_ARGUMENT, "session is NULL");
   return dflow::session_stats(s, out);

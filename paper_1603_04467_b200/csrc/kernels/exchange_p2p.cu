@@ -32,12 +32,15 @@ __device__ __forceinline__ void block_wait_flags(const uint32_t* flags, int n, u
   __syncthreads();
 }
 
-// Every thread fences its peer stores; the last block to finish raises `phase` flags
-// flags[j][phase][rank] = epoch on every rank j.
+// The block's peer stores are ordered before thread 0 by the CTA barrier; thread 0's
+// system-scope fence is cumulative over them (one fence per block, not per thread: a
+// per-thread fence.sc.sys waits out every thread's own NVLink stores and cost ~30 us per
+// db pass).  The last block to finish raises `phase` flags flags[j][phase][rank] = epoch
+// on every rank j.
 __device__ __forceinline__ void grid_signal(const P2PLayer& p, int phase, uint32_t epoch) {
-  __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {
+    __threadfence_system();
     const int prev = atomicAdd(&p.done[phase], 1);
     if (prev == static_cast<int>(gridDim.x) - 1) {
       p.done[phase] = 0;

@@ -768,7 +768,15 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
                                          static_cast<__nv_bfloat16*>(s->A0.hi), s->ld_A0, rows, in, st);
   tend(s, t, st);
   ST(check_launch(s, e, 1, "input cast"));
-  for (int l = 0; l + 1 < s->L; ++l) ST(launch_gemm(s, s->layers[l].fwd, st));
+  // defer_apply: layer l's update of the previous step may still be in flight on the
+  // exchange stream; each GEMM waits for exactly the parameters it reads
+  const bool pending = s->apply_pending;
+  s->apply_pending = false;
+  for (int l = 0; l + 1 < s->L; ++l) {
+    if (pending) CU(cudaStreamWaitEvent(st, s->ev_apply[l], 0));
+    ST(launch_gemm(s, s->layers[l].fwd, st));
+  }
+  if (pending) CU(cudaStreamWaitEvent(st, s->ev_apply[s->L - 1], 0));
   // last layer: Relu + loss seed (+ db_L partials) fused into the GEMM epilogue (a1+a2+a5)
   Layer& last = s->layers[s->L - 1];
   const bool need_y = s->loss_kind == DFLOW_LOSS_MSE;
@@ -892,9 +900,22 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     return DFLOW_OK;
   }
   const bool t16 = mode == 0 && s->replicas > 1 && u16_wire(s);
-  for (int l = s->L - 1; l >= 0; --l) {
+  // defer_apply: the order L..1 with the last two dW swapped — ..., dgrad(2), dW_1, dW_2 —
+  // so layer 1's exchange runs under dW_2 and layer 2's (the last) under the next step's
+  // forward of layer 1; the step does not join the exchange stream.  dgrad(l) still reads
+  // W_l before this rank's dW_l contribution can let an owner overwrite it.  (Running every
+  // dgrad first and the dW in order 1..L hides the same tail but puts each exchange under a
+  // dW GEMM's own NVLink stores: measured slower at N = 4.)
+  const bool defer = mode == 0 && s->defer && s->L >= 2;
+  for (int i = 0; i < s->L; ++i) {
+    int l = s->L - 1 - i;
+    if (defer && l <= 1) l = 1 - l;  // positions L-2, L-1 run layers 0, 1 (0-based)
     Layer& ly = s->layers[l];
-    if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
+    if (!defer || l >= 2) {
+      if (l > 0) ST(launch_gemm(s, ly.dgrad, st));
+    } else if (l == 0) {
+      ST(launch_gemm(s, s->layers[1].dgrad, st));  // dZ_1 for dW_1 (layer 1's dgrad, 0-based)
+    }
     const bool p2p = t16 && s->p2p;
     const Round16 send_code = round16_of(s, l, 0);  // this rank's coding of its gradient (a6)
     GemmPlan& wp = p2p ? ly.wgrad_p2p
@@ -913,7 +934,16 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
     if (mode == 0) ST(exchange_apply(s, l, st));
   }
-  if (mode == 0 && s->replicas > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
+  if (defer) s->apply_pending = true;  // joined per layer by the next forward
+  else if (mode == 0 && s->replicas > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
+  return DFLOW_OK;
+}
+
+// Orders st after every pending update (defer_apply).
+dflow_status join_apply(dflow_session* s, cudaStream_t st) {
+  if (!s->apply_pending) return DFLOW_OK;
+  for (int l = 0; l < s->L; ++l) CU(cudaStreamWaitEvent(st, s->ev_apply[l], 0));
+  s->apply_pending = false;
   return DFLOW_OK;
 }
 
@@ -1121,6 +1151,7 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
     delete s;
     return fail(DFLOW_INVALID_ARGUMENT, "async_dp supports up to %d ranks", kMaxRanks);
   }
+  s->defer = opt.defer_apply != 0 && !s->async && !s->mp && opt.world > 1;
   s->p2p = !s->async && !s->mp && opt.p2p && opt.world > 1 &&
            (opt.exchange == DFLOW_EXCHANGE_TRUNC16 || opt.exchange == DFLOW_EXCHANGE_SR16);
   dflow_status st = insert_exchange(user, s->replicas, opt.exchange | (s->async ? DFLOW_EXCHANGE_ASYNC : 0), &s->g,
@@ -1428,6 +1459,7 @@ dflow_status session_variable_assign(dflow_session* s, dflow_node var, const voi
   const int l = layer_of_variable(s, s->remap[var], &is_bias);
   if (l < 0) return fail(DFLOW_INVALID_ARGUMENT, "node is not a Variable of the planned MLP");
   cudaSetDevice(s->opt.device);
+  ST(join_apply(s, st));
   Layer& ly = s->layers[l];
   float* dst = is_bias ? ly.b32 : ly.W32;
   const size_t bytes = (is_bias ? ly.out : ly.in * ly.out) * sizeof(float);
@@ -1456,6 +1488,7 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
   const int l = layer_of_variable(s, s->remap[var], &is_bias);
   if (l < 0) return fail(DFLOW_INVALID_ARGUMENT, "node is not a Variable of the planned MLP");
   cudaSetDevice(s->opt.device);
+  ST(join_apply(s, st));
   Layer& ly = s->layers[l];
   if (s->async) ST(async_pull(s, st));  // the shared parameters, not this replica's last pull
   if (s->p2p && ly.p2p.owner_apply && !is_bias)  // owner-apply: other shards live with their owners
@@ -1482,6 +1515,7 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
   if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
   const int N = s->opt.world;
   cudaSetDevice(s->opt.device);
+  ST(join_apply(s, st));
   if (N == 1 || s->opt.exchange == DFLOW_EXCHANGE_NONE) {  // no channel, no codec (reading A6)
     CU(cudaMemcpyAsync(out, grad, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
     return DFLOW_OK;
@@ -1538,6 +1572,12 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
   CU(cudaEventRecord(s->ev_loss, cs));
   CU(cudaStreamWaitEvent(st, s->ev_loss, 0));
   return DFLOW_OK;
+}
+
+dflow_status session_sync(dflow_session* s, cudaStream_t st) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  cudaSetDevice(s->opt.device);
+  return join_apply(s, st);
 }
 
 dflow_status session_stats(dflow_session* s, dflow_stats* out) {

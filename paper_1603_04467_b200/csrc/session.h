@@ -95,6 +95,10 @@ struct dflow_session {
   size_t host_stage_bytes[2] = {0, 0};
   cudaStream_t comm = nullptr;
   std::vector<cudaEvent_t> ev_grad, ev_apply;
+  // opt.defer_apply: layer l's update (ev_apply[l], comm stream) not yet joined by any
+  // stream; the next forward waits per layer, every other entry point joins all
+  bool defer = false;
+  bool apply_pending = false;
   cudaEvent_t ev_loss = nullptr;
   cudaEvent_t ev_loss_ready = nullptr;  // loss value landed in loss_host (after the forward)
   bool loss_pending = false;
@@ -167,4 +171,5 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
 dflow_status session_async_pull(dflow_session* s, cudaStream_t st);
 dflow_status session_exchange(dflow_session* s, const float* grad, float* out, size_t n, cudaStream_t st);
 dflow_status session_stats(dflow_session* s, dflow_stats* out);
+dflow_status session_sync(dflow_session* s, cudaStream_t st);
 }  // namespace dflow

@@ -25,14 +25,15 @@ class Run:
 
     def __init__(self, dims, loss="MSE", lr=0.25, rows=256, exchange="TRUNC16", world=1, rank=0, device=0,
                  with_dx=False, nccl_id=None, overlap=1, sm_reserve=0, train=True, precision="bf16", p2p=0,
-                 sr_seed=0, graphs=0, async_dp=0, model_parallel=0):
+                 sr_seed=0, graphs=0, async_dp=0, model_parallel=0, defer_apply=0):
         self.mlp = D.mlp_graph(dims, loss, lr, with_dx=with_dx, train=train)
         self.dims = tuple(dims)
         self.loss = loss
         prec = D.DFLOW_PRECISION_3XTF32 if precision == "3xtf32" else D.DFLOW_PRECISION_BF16
         opts = D.make_options(world=world, rank=rank, device=device, exchange=exchange, max_local_rows=rows,
                               overlap=overlap, sm_reserve=sm_reserve, precision=prec, p2p=p2p, sr_seed=sr_seed,
-                              graphs=graphs, async_dp=async_dp, model_parallel=model_parallel)
+                              graphs=graphs, async_dp=async_dp, model_parallel=model_parallel,
+                              defer_apply=defer_apply)
         self.s = D.session_create(self.mlp, opts, nccl_id)
 
     def close(self):

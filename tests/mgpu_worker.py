@@ -31,7 +31,10 @@ import synth  # noqa: E402
 
 def main(out_path, exchange):
     p2p = 0
+    defer = 0
     precision = "bf16"
+    if exchange.endswith("_DEFER"):  # options.defer_apply: the same bits as the eager join
+        exchange, defer = exchange[:-6], 1
     if exchange.endswith("_TF32"):  # the fp32-faithful 3xTF32 path over the same channel
         exchange, precision = exchange[:-5], "3xtf32"
     if exchange.endswith("_P2P"):  # the fused NVLink exchange (f1): same bits as the NCCL path
@@ -46,7 +49,7 @@ def main(out_path, exchange):
         idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(idt, 0)
     nid = bytes(idt.cpu().numpy().tobytes())
-    verdict = {"world": world, "exchange": exchange, "p2p": p2p}
+    verdict = {"world": world, "exchange": exchange, "p2p": p2p, "defer_apply": defer}
 
     w = synth.with_batch(synth.C2, 256)
     b = w.batch // world
@@ -54,7 +57,7 @@ def main(out_path, exchange):
     X, Y = synth.batch(w)
     Xr, Yr = X[rank * b:(rank + 1) * b], Y[rank * b:(rank + 1) * b]
     run = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local, nccl_id=nid,
-              p2p=p2p, sr_seed=seed, precision=precision)
+              p2p=p2p, sr_seed=seed, precision=precision, defer_apply=defer)
     verdict["precision"] = precision
     run.assign(Ws, bs)
     Xd, Yd = torch.from_numpy(Xr).cuda(), torch.from_numpy(Yr).cuda()
@@ -138,6 +141,26 @@ def main(out_path, exchange):
     dist.all_gather(allW, mt)
     verdict["p11_after_4_steps"] = all(bool(torch.equal(allW[0], x)) for x in allW)
     run.close()
+    if defer:
+        # the same 4 steps with the eager join (defer_apply = 0): bit-identical parameters
+        # (a second communicator needs its own NCCL id)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid2 = bytes(idt.cpu().numpy().tobytes())
+        eager = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local,
+                    nccl_id=nid2, p2p=p2p, sr_seed=seed, precision=precision, defer_apply=0)
+        eager.assign(Ws, bs)
+        gW, gb, _ = eager.gradients(Xd, Yd)  # the same call sequence (SR16 draws are keyed by step)
+        eager.step(Xd, Yd)
+        for step in range(3):
+            Xs, Ys = synth.batch(w, step=step)
+            eager.step(torch.from_numpy(Xs[rank * b:(rank + 1) * b]).cuda(),
+                       torch.from_numpy(Ys[rank * b:(rank + 1) * b]).cuda())
+        We, be = eager.read()
+        verdict["defer_equals_eager"] = all(bool(np.array_equal(a.view(np.uint32), c.view(np.uint32)))
+                                            for a, c in zip(We + be, Wg + bg))
+        eager.close()
     if rank == 0:
         with open(out_path, "w") as f:
             json.dump(verdict, f)

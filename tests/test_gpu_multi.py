@@ -36,7 +36,8 @@ def _run(n, exchange, tmp_path):
 
 
 @pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL", "SR16", "SR16_P2P",
-                                      "TRUNC16_P2P_TF32", "FP32_TF32"])
+                                      "TRUNC16_P2P_TF32", "FP32_TF32", "TRUNC16_P2P_DEFER",
+                                      "TRUNC16_DEFER"])
 def test_two_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 2:
@@ -51,9 +52,11 @@ def test_two_gpu_replicated_step(exchange, tmp_path):
     # codec's two truncations (2^-7 each) dominate, so the bf16-level gate applies
     tol = 1e-4 if exchange == "FP32_TF32" else 2e-2
     assert v["w_after_max_err"] < tol, v
+    if exchange.endswith("_DEFER"):
+        assert v["defer_equals_eager"], v
 
 
-@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "SR16_P2P"])
+@pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "SR16_P2P", "TRUNC16_P2P_DEFER"])
 def test_four_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 4:
@@ -62,3 +65,5 @@ def test_four_gpu_replicated_step(exchange, tmp_path):
     print(v)
     assert v["p4_exchange_ok"] and v["p4_step_bitexact"] and v["p11_after_4_steps"], v
     assert v["w_after_max_err"] < 2e-2, v
+    if exchange.endswith("_DEFER"):
+        assert v["defer_equals_eager"], v
