@@ -50,31 +50,35 @@ __device__ __forceinline__ void grid_signal(const P2PLayer& p, int phase, uint32
   }
 }
 
+// One thread per column, no shared memory (so it fits beside a running GEMM CTA on the
+// exchange stream): the same summation order as k_colsum_final — eight interleaved
+// partial sums t_g over chunks k = g, g+8, ... (left folds), then t_0 + ... + t_7 — so db
+// is bit-identical to the fetched gradient's.
 __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int64_t cols, int64_t base_idx,
                                    const P2PLayer p, uint32_t epoch, Round16 r16) {
-  __shared__ float sm[8][33];
-  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t c = blockIdx.x * 32LL + cl;
-  float t = 0.f;
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (c < cols) {
-    int k = g;
-    for (; k + 24 < chunks; k += 32) {
-      const float a0 = ws[(int64_t)k * cols + c], a1 = ws[(int64_t)(k + 8) * cols + c];
-      const float a2 = ws[(int64_t)(k + 16) * cols + c], a3 = ws[(int64_t)(k + 24) * cols + c];
-      t = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(t, a0), a1), a2), a3);
-    }
-    for (; k < chunks; k += 8) t = __fadd_rn(t, ws[(int64_t)k * cols + c]);
-  }
-  sm[g][cl] = t;
-  __syncthreads();
-  if (g == 0 && c < cols) {
-    float s = sm[0][cl];
+    float t[8];
 #pragma unroll
-    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
+    for (int g = 0; g < 8; ++g) t[g] = 0.f;
+    int k0 = 0;
+    for (; k0 + 8 <= chunks; k0 += 8) {  // 8 independent loads in flight
+      float a[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) a[g] = ws[static_cast<int64_t>(k0 + g) * cols + c];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) t[g] = __fadd_rn(t[g], a[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (k0 + g < chunks) t[g] = __fadd_rn(t[g], ws[static_cast<int64_t>(k0 + g) * cols + c]);
+    float sum = t[0];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) sum = __fadd_rn(sum, t[g]);
     const int64_t idx = base_idx + c;
     const int owner = static_cast<int>(idx / p.shard);
     p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
-        static_cast<uint16_t>(round16(__float_as_uint(s), idx, r16));
+        static_cast<uint16_t>(round16(__float_as_uint(sum), idx, r16));
   }
   grid_signal(p, 0, epoch);
 }
@@ -180,8 +184,8 @@ __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
 
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
                                     uint32_t epoch, cudaStream_t s, Round16 r) {
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 31) / 32));
-  k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64));
+  k_colsum_final_p2p<<<blocks, 64, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);
   return cudaGetLastError();
 }
 

@@ -806,7 +806,8 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
 }
 
 // Exchange + apply of layer l (comm stream when N > 1).
-dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
+// joined: the exchange stream already waits for this layer's gradient (ev_grad[l]).
+dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st, bool joined) {
   Layer& ly = s->layers[l];
   const int N = s->replicas;
   const int64_t nW = ly.in * ly.out;
@@ -815,8 +816,10 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st) {
   const float* g32 = ly.g32;
   if (N > 1) {
     cs = s->comm;
-    CU(cudaEventRecord(s->ev_grad[l], st));
-    CU(cudaStreamWaitEvent(cs, s->ev_grad[l], 0));
+    if (!joined) {
+      CU(cudaEventRecord(s->ev_grad[l], st));
+      CU(cudaStreamWaitEvent(cs, s->ev_grad[l], 0));
+    }
     const int t = tbegin(s, 2, cs);
     const Round16 own_code = round16_of(s, l, 1);  // the owner's coding of the mean (a8)
     switch (s->opt.exchange) {
@@ -922,17 +925,25 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
                        : t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32);
     wp.args.r16 = send_code;
     ST(launch_gemm(s, wp, st));
-    // db_l: the producing epilogue left per-32-row column partials; sum them in order
-    const int t = tbegin(s, 1, st);
+    // db_l: the producing epilogue left per-32-row column partials; sum them in order.
+    // N > 1: on the exchange stream, under the next dgrad (it only feeds the exchange)
+    const bool on_comm = mode == 0 && s->replicas > 1;
+    cudaStream_t cst = st;
+    if (on_comm) {
+      CU(cudaEventRecord(s->ev_grad[l], st));
+      CU(cudaStreamWaitEvent(s->comm, s->ev_grad[l], 0));
+      cst = s->comm;
+    }
+    const int t = tbegin(s, 1, cst);
     const int chunks = static_cast<int>((rows + 31) / 32);
-    cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, st,
+    cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, cst,
                                                   send_code)
                         : launch_colsum_final(ly.colsum_ws, chunks, ly.out, t16 ? nullptr : ly.g32 + ly.in * ly.out,
-                                              t16 ? ly.q16 + ly.in * ly.out : nullptr, st, send_code,
+                                              t16 ? ly.q16 + ly.in * ly.out : nullptr, cst, send_code,
                                               ly.in * ly.out);
-    tend(s, t, st);
+    tend(s, t, cst);
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
-    if (mode == 0) ST(exchange_apply(s, l, st));
+    if (mode == 0) ST(exchange_apply(s, l, st, on_comm));
   }
   if (defer) s->apply_pending = true;  // joined per layer by the next forward
   else if (mode == 0 && s->replicas > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
@@ -1025,7 +1036,7 @@ dflow_status run_backward_mp(dflow_session* s, int64_t rows, cudaStream_t st) {
                                         ly.g32 + ly.in * ly.out, nullptr, st);
     tend(s, t, st);
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
-    ST(exchange_apply(s, l, st));  // replicas == 1: the bias update
+    ST(exchange_apply(s, l, st, false));  // replicas == 1: the bias update
   }
   return DFLOW_OK;
 }
