@@ -194,11 +194,15 @@ __global__ void k_loss_final(int kind, const double* __restrict__ partials, int 
   }
 }
 
+// ApplyGradientDescent: w <- fl(w - fl(lr * g))
+__device__ __forceinline__ float sgd(float w, float lr, float g) { return __fsub_rn(w, __fmul_rn(lr, g)); }
+
 // ------------------------------------------------------------------ colsum (final pass)
 // Block = 32 columns x 8 chunk-groups; group g sums chunks g, g+8, ... in order, then
 // the 8 group sums are added in group order (deterministic, ~#chunks/8 dependent adds).
 __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols, float* __restrict__ out32,
-                               uint16_t* __restrict__ out16, Round16 r16, int64_t idx_base) {
+                               uint16_t* __restrict__ out16, Round16 r16, int64_t idx_base,
+                               float* __restrict__ bias, float lr) {
   __shared__ float sm[8][33];
   const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t c = blockIdx.x * 32LL + cl;
@@ -220,6 +224,7 @@ __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t
     for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
     if (out32) out32[c] = s;
     if (out16) out16[c] = static_cast<uint16_t>(round16(__float_as_uint(s), idx_base + c, r16));
+    if (bias) bias[c] = sgd(bias[c], lr, s);  // N = 1: ApplyGradientDescent on b_l (a9), fused
   }
 }
 
@@ -295,7 +300,6 @@ __global__ void k_scale_f32(float* __restrict__ x, int64_t n, float scale) {
 }
 
 // ------------------------------------------------------------------ SGD apply
-__device__ __forceinline__ float sgd(float w, float lr, float g) { return __fsub_rn(w, __fmul_rn(lr, g)); }
 
 __global__ void k_apply_sgd_vec(float* __restrict__ W, const float* __restrict__ g32,
                                 const uint16_t* __restrict__ g16, int64_t n8, __nv_bfloat16* __restrict__ wbf,
@@ -452,10 +456,10 @@ cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t r
 }
 
 cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
-                                cudaStream_t s, Round16 r, int64_t idx_base) {
+                                cudaStream_t s, Round16 r, int64_t idx_base, float* bias, float lr) {
   if (cols == 0) return cudaSuccess;
   k_colsum_final<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16, r,
-                                                                          idx_base);
+                                                                          idx_base, bias, lr);
   return cudaGetLastError();
 }
 

@@ -38,8 +38,10 @@ cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t r
 // NK8 final pass: db[c] = sum_k ws[k, c] over the `chunks` per-32-row partial
 // column sums the dz-producing epilogue wrote (fixed order).  fp32 and/or u16 out.
 // The u16 output is round16(bits(db[c]), idx_base + c, r) (the db tail of the layer bucket).
+// bias != NULL (N = 1 train step): also bias[c] <- fl(bias[c] - fl(lr * db[c])).
 cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
-                                cudaStream_t s, Round16 r = {0, 0}, int64_t idx_base = 0);
+                                cudaStream_t s, Round16 r = {0, 0}, int64_t idx_base = 0, float* bias = nullptr,
+                                float lr = 0.f);
 
 // NK11: owner fold of N received shards (rank order), x (1/N), 16-bit code (truncate or
 // SR16 at bucket positions idx_base + i).

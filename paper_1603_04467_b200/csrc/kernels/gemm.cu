@@ -207,7 +207,7 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   if (const char* e = getenv("DFLOW_GEMM_PREFETCH")) a.prefetch = atoi(e) >= 0 ? atoi(e) : a.prefetch;
   if (const char* e = getenv("DFLOW_GEMM_DEBUG")) a.debug = atoi(e);
   a.sgd_lr = d.sgd_lr;
-  a.sched = default_sched();
+  a.sched = d.sched ? d.sched : default_sched();
   if (!a.sched) {
     snprintf(g_err, sizeof g_err, "could not allocate the tile-scheduler counters");
     return cudaErrorMemoryAllocation;

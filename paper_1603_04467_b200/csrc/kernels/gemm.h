@@ -102,6 +102,8 @@ struct GemmDesc {
   int group;       // tile-raster group (M tiles); 0 = default
   int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)
+  int* sched;      // tile-scheduler counters [2] (zeroed); NULL = the per-device default.
+                   // GEMMs that may run concurrently must not share counters
 };
 
 // Prepared launch: tensor maps + args, reusable across calls while buffers stay put.

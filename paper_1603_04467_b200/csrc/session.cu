@@ -391,6 +391,12 @@ dflow_status alloc_state(dflow_session* s) {
   cudaEventCreateWithFlags(&s->ev_feeds_free, cudaEventDisableTiming);
   if (cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking) != cudaSuccess)
     return fail(DFLOW_CUDA, "stream creation failed");
+  for (int i = 0; i < 2; ++i) {
+    if (cudaStreamCreateWithFlags(&s->side[i], cudaStreamNonBlocking) != cudaSuccess)
+      return fail(DFLOW_CUDA, "stream creation failed");
+    cudaEventCreateWithFlags(&s->ev_side_join[i], cudaEventDisableTiming);
+  }
+  ST(dmalloc(s, &s->sched_w, 4));  // zeroed
   return DFLOW_OK;
 }
 
@@ -622,6 +628,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     w.epilogue = EPI_F32;
     w.out_f32 = ly.g32; w.ldo32 = ly.out;
     w.max_ctas = max_ctas;
+    w.sched = s->sched_w + 2 * (l % 2);  // (bwd_side: dW_l runs on side[l % 2])
     ST(gemm_plan(s, w, &ly.wgrad32));
     if (s->replicas == 1 && s->trainable) {
       // no channel (reading A6): ApplyGradientDescent fused into the dW epilogue
@@ -666,6 +673,14 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       ly.has_wgrad_p2p = true;
     }
   }
+  // N = 1: can the dW GEMMs run beside the dgrads (and each other) without queueing for SMs?
+  int wsum = 0, dmax = 0;
+  for (int l = 0; l < s->L; ++l) {
+    const Layer& ly = s->layers[l];
+    wsum += ly.has_wgrad_apply ? ly.wgrad_apply.grid : ly.wgrad32.grid;
+    if (ly.has_dgrad) dmax = std::max(dmax, ly.dgrad.grid);
+  }
+  s->bwd_side = s->replicas == 1 && !s->mp && s->L > 1 && wsum + dmax <= s->num_sms;
   s->planned_rows = rows;
   return DFLOW_OK;
 }
@@ -924,11 +939,20 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     GemmPlan& wp = p2p ? ly.wgrad_p2p
                        : t16 ? ly.wgrad16 : (mode == 0 && ly.has_wgrad_apply ? ly.wgrad_apply : ly.wgrad32);
     wp.args.r16 = send_code;
-    ST(launch_gemm(s, wp, st));
+    // small N = 1 steps: dW_l (+ its update) and db_l beside dgrad(l-1) on the side stream
+    // (dgrad(l), which reads W_l, is already enqueued before the fork)
+    const bool side = mode == 0 && s->bwd_side;
+    cudaStream_t wst = st;
+    if (side) {
+      CU(cudaEventRecord(s->ev_grad[l], st));
+      CU(cudaStreamWaitEvent(s->side[l % 2], s->ev_grad[l], 0));
+      wst = s->side[l % 2];
+    }
+    ST(launch_gemm(s, wp, wst));
     // db_l: the producing epilogue left per-32-row column partials; sum them in order.
     // N > 1: on the exchange stream, under the next dgrad (it only feeds the exchange)
     const bool on_comm = mode == 0 && s->replicas > 1;
-    cudaStream_t cst = st;
+    cudaStream_t cst = wst;
     if (on_comm) {
       CU(cudaEventRecord(s->ev_grad[l], st));
       CU(cudaStreamWaitEvent(s->comm, s->ev_grad[l], 0));
@@ -936,14 +960,23 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     }
     const int t = tbegin(s, 1, cst);
     const int chunks = static_cast<int>((rows + 31) / 32);
+    // N = 1: W was updated by the dW epilogue; the b_l update rides on this pass too
+    const bool fused_b = mode == 0 && s->replicas == 1 && ly.has_wgrad_apply;
     cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, cst,
                                                   send_code)
-                        : launch_colsum_final(ly.colsum_ws, chunks, ly.out, t16 ? nullptr : ly.g32 + ly.in * ly.out,
+                        : launch_colsum_final(ly.colsum_ws, chunks, ly.out,
+                                              (t16 || fused_b) ? nullptr : ly.g32 + ly.in * ly.out,
                                               t16 ? ly.q16 + ly.in * ly.out : nullptr, cst, send_code,
-                                              ly.in * ly.out);
+                                              ly.in * ly.out, fused_b ? ly.b32 : nullptr, ly.n.lr_b);
     tend(s, t, cst);
     ST(check_launch(s, e, 1, "bias-gradient column sum"));
-    if (mode == 0) ST(exchange_apply(s, l, st, on_comm));
+    if (mode == 0 && !fused_b) ST(exchange_apply(s, l, st, on_comm));
+  }
+  if (mode == 0 && s->bwd_side) {  // join the side streams (the updates) back into st
+    for (int i = 0; i < 2; ++i) {
+      CU(cudaEventRecord(s->ev_side_join[i], s->side[i]));
+      CU(cudaStreamWaitEvent(st, s->ev_side_join[i], 0));
+    }
   }
   if (defer) s->apply_pending = true;  // joined per layer by the next forward
   else if (mode == 0 && s->replicas > 1) CU(cudaStreamWaitEvent(st, s->ev_apply[0], 0));
@@ -1231,6 +1264,7 @@ void session_destroy(dflow_session* s) {
   }
   free_operand(s->A0);
   if (s->mp_recv) cudaFree(s->mp_recv);
+  if (s->sched_w) cudaFree(s->sched_w);
   for (void* p : {(void*)s->AL32, (void*)s->loss_partials, (void*)s->loss_dev, (void*)s->mask_dev, s->host_stage[0],
                   s->host_stage[1], s->xbuf[0], s->xbuf[1], s->xbuf[2], s->xbuf[3]})
     if (p) cudaFree(p);
@@ -1244,6 +1278,10 @@ void session_destroy(dflow_session* s) {
     if (e) cudaEventDestroy(e);
   if (s->gstream) cudaStreamDestroy(s->gstream);
   if (s->h2d) cudaStreamDestroy(s->h2d);
+  for (int i = 0; i < 2; ++i) {
+    if (s->side[i]) cudaStreamDestroy(s->side[i]);
+    if (s->ev_side_join[i]) cudaEventDestroy(s->ev_side_join[i]);
+  }
   if (s->comm) cudaStreamDestroy(s->comm);
   cudaGetLastError();
   delete s;

@@ -99,6 +99,12 @@ struct dflow_session {
   // stream; the next forward waits per layer, every other entry point joins all
   bool defer = false;
   bool apply_pending = false;
+  // N = 1, small layers (all dW grids + the largest dgrad grid <= #SMs): dW_l and db_l run
+  // on side[l % 2], concurrently with the next dgrad and with dW_{l-1} (no shared buffers)
+  cudaStream_t side[2] = {nullptr, nullptr};
+  cudaEvent_t ev_side_join[2] = {nullptr, nullptr};
+  int* sched_w = nullptr;  // [2][2] tile-scheduler counters of the dW GEMMs, per side stream
+  bool bwd_side = false;
   cudaEvent_t ev_loss = nullptr;
   cudaEvent_t ev_loss_ready = nullptr;  // loss value landed in loss_host (after the forward)
   bool loss_pending = false;
