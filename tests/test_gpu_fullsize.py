@@ -72,3 +72,56 @@ def test_c3_full_batch_sampled_parity():
             assert np.array_equal(ba[l], expb), l
     finally:
         run.close()
+
+
+def test_c5_full_batch_sampled_parity():
+    """C5 (16 x 4096^2, B = 65536, the fp32-faithful 3xTF32 path) at full size on one GPU:
+    sampled forward rows and dW_L entries against f64 recomputations from the exact fp32
+    values the GPU stores (tf32 pairs join exactly, reading A14), gated at the north star's
+    1e-4 relative to the |terms| bound; the update element by element (reading A9)."""
+    assert torch.cuda.is_available()
+    w = synth.C5
+    rows = w.batch
+    L = w.layers
+    Ws, bs = synth.init_params(w)
+    X, Y = synth.batch(w)
+    run = Run(w.dims, "MSE", w.lr, rows=rows, precision="3xtf32")
+    try:
+        run.assign(Ws, bs)
+        Xd, Yd = torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda()
+        g = np.random.default_rng(6)
+        # ---- forward, layer 1, sampled rows: fp32-faithful, so f64 of the fp32 inputs
+        A1 = run.forward(Xd, Yd, fetch=run.mlp.relus[0])
+        rs = g.choice(rows, 8, replace=False)
+        x64, w64 = X[rs].astype(np.float64), Ws[0].astype(np.float64)
+        z = x64 @ w64 + bs[0].astype(np.float64)
+        bound = np.abs(x64) @ np.abs(w64) + np.abs(bs[0]).astype(np.float64)
+        err = np.abs(A1[rs] - np.maximum(z, 0)) / bound
+        assert np.max(err) < 1e-5, float(np.max(err))
+        del A1
+        # ---- dW_L sampled entries over the full batch (K = 65536)
+        Aprev = run.forward(Xd, Yd, fetch=run.mlp.relus[L - 2])   # fp32 A_{L-1} (hi + lo)
+        AL = run.forward(Xd, Yd, fetch=run.mlp.relus[L - 1])      # fp32 A_L
+        gW, gb, _ = run.gradients(Xd, Yd)
+        d = (AL - Y) / np.float32(rows * w.dims[-1])               # (a - y) / 2^28: exact scaling
+        dZ = np.where(AL > 0, d, np.float32(0)).astype(np.float64)
+        ii = g.choice(w.dims[L - 1], 16, replace=False)
+        jj = g.choice(w.dims[L], 16, replace=False)
+        ref = Aprev[:, ii].astype(np.float64).T @ dZ[:, jj]
+        bound = np.abs(Aprev[:, ii]).astype(np.float64).T @ np.abs(dZ[:, jj])
+        got = gW[L - 1][np.ix_(ii, jj)]
+        rel = np.abs(got - ref) / (bound + 1e-300)
+        assert np.max(rel) < 1e-4, float(np.max(rel))
+        refb = dZ[:, jj].sum(0)
+        assert np.allclose(gb[L - 1][jj], refb, rtol=1e-5, atol=1e-5 * np.abs(dZ[:, jj]).sum(0).max())
+        del Aprev, AL
+        # ---- the update: W_after == fl(W - fl(lr * dW)) for every element (N = 1: no codec)
+        run.step(Xd, Yd)
+        Wa, ba = run.read()
+        for l in range(L):
+            exp = OK.apply_gradient_descent(Ws[l], w.lr, gW[l], "f32")
+            assert np.array_equal(Wa[l], exp), l
+            expb = OK.apply_gradient_descent(bs[l], w.lr, gb[l], "f32")
+            assert np.array_equal(ba[l], expb), l
+    finally:
+        run.close()
