@@ -430,7 +430,7 @@ def main():
     ap.add_argument("--async-dp", type=int, default=0,
                     help="N > 1: 1 = asynchronous replicas (f3): each rank pulls the shared parameters, steps "
                          "and pushes its own coded update with no barrier (the exchange names the coding)")
-    ap.add_argument("--defer-apply", type=int, default=0,
+    ap.add_argument("--defer-apply", type=int, default=1,
                     help="N > 1 synchronous: last two dW swapped, layer l's update joined only by the next "
                          "forward of layer l (options.defer_apply; same bits)")
     ap.add_argument("--sm-reserve", type=int, default=0)

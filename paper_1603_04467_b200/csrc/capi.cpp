@@ -312,6 +312,9 @@ dflow_status dflow_fetch_relu_masks(dflow_session* s, int layer, uint32_t* out_b
 dflow_status dflow_session_set_timing(dflow_session* s, int enable) {
   if (!s) return fail(DFLOW_INVALID_ARGUMENT, "session is NULL");
   s->timing = enable != 0;
+  s->ranges.clear();  // (a partial DFLOW_TIMING_BATCH window is dropped)
+  s->event_next = 0;
+  s->timing_pending = 0;
   s->gemm_ms = s->other_ms = s->exchange_ms = 0;
   s->timed_steps = 0;
   return DFLOW_OK;

@@ -1357,8 +1357,17 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   CU(cudaGetLastError());
   ST(wait_loss(s, loss_out));
   if (s->timing) {
-    ST(finish_timing(s, st));
-    s->timed_steps++;
+    // DFLOW_TIMING_BATCH=k: read the events back every k steps only, so the timeline
+    // (DFLOW_TIMELINE) shows k consecutive steps running back to back, overlaps included
+    static const int batch = [] {
+      const char* e = getenv("DFLOW_TIMING_BATCH");
+      return (e && atoi(e) > 1) ? atoi(e) : 1;
+    }();
+    if (++s->timing_pending >= batch) {
+      ST(finish_timing(s, st));
+      s->timed_steps += s->timing_pending;
+      s->timing_pending = 0;
+    }
   }
   return DFLOW_OK;
 }

@@ -147,6 +147,7 @@ struct dflow_session {
   int64_t last_rows = 0;
   // timing / stats
   bool timing = false;
+  int timing_pending = 0;  // steps whose events are not read back yet (DFLOW_TIMING_BATCH)
   std::vector<dflow::TimedRange> ranges;
   std::vector<cudaEvent_t> event_pool;
   size_t event_next = 0;
