@@ -214,6 +214,18 @@ dflow_status dflow_train_step(dflow_session* s, int n_feeds, const dflow_node* f
 dflow_status dflow_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                    const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
                                    float* loss_out, void* stream);
+/* Pipelined end-to-end step: the same step, but the call returns as soon as the uploads and
+ * the step are enqueued, so the host can enqueue step i+1 while step i runs and the PCIe link
+ * stays busy (x of step i+1 uploads as soon as step i's input cast has read its staging
+ * buffer, y as soon as step i's loss GEMM has).  Every step still copies its loss to the host;
+ * *prev_loss_out receives the loss of the PREVIOUS pipelined call (*has_loss = 1; 0 on the
+ * first call), which that step's forward produced.  host_ptrs of a call must stay unchanged
+ * until the next pipelined call (or dflow_session_last_loss) returns.                      */
+dflow_status dflow_train_step_host_pipelined(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                             const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
+                                             float* prev_loss_out, int32_t* has_loss, void* stream);
+/* Waits for and returns the loss of the last pipelined host step (*has_loss = 0 if none). */
+dflow_status dflow_session_last_loss(dflow_session* s, float* loss_out, int32_t* has_loss);
 /* async_dp sessions: this replica's local parameters (and operand copies) <- the current
  * shared shards of every rank (NVLink loads), stream-ordered on `stream`.  The updates
  * other replicas push concurrently may or may not be included (no lock, reading A29). */

@@ -86,6 +86,9 @@ _SIGS = {
     "dflow_variable_read": (_i32, [_p, _node, _p, _i32, _p]),
     "dflow_train_step": (_i32, [_p, _i32, _pnode, C.POINTER(_p), _pi64, _i64, C.POINTER(C.c_float), _p]),
     "dflow_train_step_host": (_i32, [_p, _i32, _pnode, C.POINTER(_p), _pi64, _i64, C.POINTER(C.c_float), _p]),
+    "dflow_train_step_host_pipelined": (_i32, [_p, _i32, _pnode, C.POINTER(_p), _pi64, _i64, C.POINTER(C.c_float),
+                                               C.POINTER(C.c_int32), _p]),
+    "dflow_session_last_loss": (_i32, [_p, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
     "dflow_forward": (_i32, [_p, _i32, _pnode, C.POINTER(_p), _pi64, _i64, _node, _p, _p]),
     "dflow_fetch_gradients": (_i32, [_p, _i32, _pnode, C.POINTER(_p), _pi64, _i64, _i32, _pnode, C.POINTER(_p), _p]),
     "dflow_fetch_relu_masks": (_i32, [_p, _i32, C.POINTER(C.c_uint32)]),

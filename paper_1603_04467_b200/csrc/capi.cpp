@@ -283,6 +283,23 @@ dflow_status dflow_train_step_host(dflow_session* s, int n_feeds, const dflow_no
   GUARD_END
 }
 
+dflow_status dflow_train_step_host_pipelined(dflow_session* s, int n_feeds, const dflow_node* feeds,
+                                             const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
+                                             float* prev_loss_out, int32_t* has_loss, void* stream) {
+  GUARD_BEGIN
+  if (!s) return fail(DFLOW_INVALID_ARGUMENT, "session is NULL");
+  return dflow::session_train_step_host(s, n_feeds, feeds, host_ptrs, ld, local_rows, prev_loss_out,
+                                        static_cast<cudaStream_t>(stream), true, has_loss);
+  GUARD_END
+}
+
+dflow_status dflow_session_last_loss(dflow_session* s, float* loss_out, int32_t* has_loss) {
+  GUARD_BEGIN
+  if (!s) return fail(DFLOW_INVALID_ARGUMENT, "session is NULL");
+  return dflow::session_last_loss(s, loss_out, has_loss);
+  GUARD_END
+}
+
 dflow_status dflow_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* dev_ptrs,
                            const int64_t* ld, int64_t local_rows, dflow_node fetch, void* out_dev, void* stream) {
   GUARD_BEGIN

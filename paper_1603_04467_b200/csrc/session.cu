@@ -56,6 +56,7 @@ inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 int tbegin(dflow_session* s, int kind, cudaStream_t st);
 void tend(dflow_session* s, int idx, cudaStream_t st);
 dflow_status check_launch(dflow_session* s, cudaError_t e, int count, const char* what);
+cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st);
 
 // Gradients cross the channel as 16-bit codes (TRUNC16 or SR16).
 inline bool u16_wire(const dflow_session* s) {
@@ -381,7 +382,9 @@ dflow_status alloc_state(dflow_session* s) {
     cudaEventCreateWithFlags(&s->ev_apply[l], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&s->ev_loss, cudaEventDisableTiming);
-  cudaEventCreateWithFlags(&s->ev_loss_ready, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_loss_ready[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_loss_ready[1], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&s->ev_x_free, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&s->ev_h2d_y, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&s->ev_gin, cudaEventDisableTiming);
@@ -783,6 +786,7 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
                                          static_cast<__nv_bfloat16*>(s->A0.hi), s->ld_A0, rows, in, st);
   tend(s, t, st);
   ST(check_launch(s, e, 1, "input cast"));
+  CU(record_event(s, s->ev_x_free, st));  // (a host-fed pipelined step may upload the next x now)
   // defer_apply: layer l's update of the previous step may still be in flight on the
   // exchange stream; each GEMM waits for exactly the parameters it reads
   const bool pending = s->apply_pending;
@@ -1121,30 +1125,31 @@ cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st) {
 dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
   if (s->mp) {  // f4: the last rank computed C; every rank reports it
     NC(ncclBroadcast(s->loss_dev, s->loss_dev, 1, ncclFloat32, s->opt.world - 1, s->nccl, st));
-    CU(cudaMemcpyAsync(s->loss_host, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
-    CU(record_event(s, s->ev_loss_ready, st));
-    s->loss_pending = true;
+    CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    CU(record_event(s, s->ev_loss_ready[s->loss_slot], st));
+    s->loss_pending[s->loss_slot] = true;
     return DFLOW_OK;
   }
   if (s->replicas > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
     CU(cudaEventRecord(s->ev_loss, st));
     CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
     NC(ncclAllReduce(s->loss_dev, s->loss_dev + 1, 1, ncclFloat32, ncclSum, s->nccl, s->comm));
-    CU(cudaMemcpyAsync(s->loss_host, s->loss_dev + 1, sizeof(float), cudaMemcpyDeviceToHost, s->comm));
-    CU(cudaEventRecord(s->ev_loss_ready, s->comm));
+    CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev + 1, sizeof(float), cudaMemcpyDeviceToHost,
+                       s->comm));
+    CU(cudaEventRecord(s->ev_loss_ready[s->loss_slot], s->comm));
   } else {
-    CU(cudaMemcpyAsync(s->loss_host, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
-    CU(record_event(s, s->ev_loss_ready, st));
+    CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
+    CU(record_event(s, s->ev_loss_ready[s->loss_slot], st));
   }
-  s->loss_pending = true;
+  s->loss_pending[s->loss_slot] = true;
   return DFLOW_OK;
 }
 
-dflow_status wait_loss(dflow_session* s, float* loss_out) {
-  if (!s->loss_pending) return DFLOW_OK;
-  s->loss_pending = false;
-  CU(cudaEventSynchronize(s->ev_loss_ready));
-  float v = s->loss_host[0];
+dflow_status wait_loss(dflow_session* s, float* loss_out, int slot) {
+  if (!s->loss_pending[slot]) return DFLOW_OK;
+  s->loss_pending[slot] = false;
+  CU(cudaEventSynchronize(s->ev_loss_ready[slot]));
+  float v = s->loss_host[slot];
   if (s->replicas > 1 && !s->async) v /= static_cast<float>(s->opt.world);
   if (loss_out) *loss_out = v;
   s->nonfinite = std::isfinite(v) ? 0 : 1;
@@ -1269,12 +1274,14 @@ void session_destroy(dflow_session* s) {
                   s->host_stage[1], s->xbuf[0], s->xbuf[1], s->xbuf[2], s->xbuf[3]})
     if (p) cudaFree(p);
   if (s->loss_host) cudaFreeHost(s->loss_host);
+  for (cudaEvent_t e : {s->ev_loss_ready[0], s->ev_loss_ready[1], s->ev_x_free})
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : s->ev_grad) cudaEventDestroy(e);
   for (cudaEvent_t e : s->ev_apply) cudaEventDestroy(e);
   for (cudaEvent_t e : s->event_pool) cudaEventDestroy(e);
   if (s->ev_loss) cudaEventDestroy(s->ev_loss);
   for (auto& g : s->step_graphs) cudaGraphExecDestroy(g.exec);
-  for (cudaEvent_t e : {s->ev_loss_ready, s->ev_h2d, s->ev_h2d_y, s->ev_feeds_free, s->ev_gin, s->ev_gout})
+  for (cudaEvent_t e : {s->ev_h2d, s->ev_h2d_y, s->ev_feeds_free, s->ev_gin, s->ev_gout})
     if (e) cudaEventDestroy(e);
   if (s->gstream) cudaStreamDestroy(s->gstream);
   if (s->h2d) cudaStreamDestroy(s->h2d);
@@ -1287,8 +1294,10 @@ void session_destroy(dflow_session* s) {
   delete s;
 }
 
-dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
-                                const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st) {
+// wait = false (pipelined host steps): the loss copy is enqueued into slot s->loss_slot and
+// left pending; the caller collects it later with wait_loss.
+dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                                     const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st, bool wait) {
   if (!s->trainable) return fail(DFLOW_UNIMPLEMENTED, "graph has no ApplyGradientDescent nodes to run");
   ST(check_rows(s, rows));
   Feeds f;
@@ -1300,6 +1309,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
     if (s->async && s->opt.async_dp == 1) ST(async_pull(s, stream));  // the replica reads the shared parameters
     if (s->mp) {  // f4: this rank's layers of the one replica
       ST(run_forward_mp(s, f, rows, stream));
+      CU(record_event(s, s->ev_x_free, stream));
       CU(record_event(s, s->ev_feeds_free, stream));
       ST(enqueue_loss(s, stream));  // every rank takes part in the loss broadcast
       ST(run_backward_mp(s, rows, stream));
@@ -1318,7 +1328,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
     const bool ywait = s->y_upload_pending;  // host-fed y: the graph holds an external wait before the last GEMM
     for (auto& e : s->step_graphs)
       if (e.x == f.x && e.y == f.y && e.ldx == f.ldx && e.ldy == f.ldy && e.rows == rows &&
-          e.loss == (loss_out != nullptr) && e.ywait == ywait)
+          e.loss == (loss_out != nullptr) && e.ywait == ywait && e.slot == s->loss_slot)
         g = &e;
     s->y_upload_pending = false;
     if (!g) {
@@ -1342,7 +1352,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
         cudaGraphExecDestroy(s->step_graphs.front().exec);
         s->step_graphs.erase(s->step_graphs.begin());
       }
-      s->step_graphs.push_back({f.x, f.y, f.ldx, f.ldy, rows, loss_out != nullptr, ywait, exec});
+      s->step_graphs.push_back({f.x, f.y, f.ldx, f.ldy, rows, loss_out != nullptr, ywait, s->loss_slot, exec});
       g = &s->step_graphs.back();
     }
     CU(cudaEventRecord(s->ev_gin, st));
@@ -1350,12 +1360,12 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
     CU(cudaGraphLaunch(g->exec, s->gstream));
     CU(cudaEventRecord(s->ev_gout, s->gstream));
     CU(cudaStreamWaitEvent(st, s->ev_gout, 0));
-    if (loss_out) s->loss_pending = true;
+    if (loss_out) s->loss_pending[s->loss_slot] = true;
   } else {
     ST(body(st));
   }
   CU(cudaGetLastError());
-  ST(wait_loss(s, loss_out));
+  if (wait) ST(wait_loss(s, loss_out, s->loss_slot));
   if (s->timing) {
     // DFLOW_TIMING_BATCH=k: read the events back every k steps only, so the timeline
     // (DFLOW_TIMELINE) shows k consecutive steps running back to back, overlaps included
@@ -1372,9 +1382,16 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
   return DFLOW_OK;
 }
 
+dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
+                                const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st) {
+  return session_train_step_impl(s, n_feeds, feeds, ptrs, ld, rows, loss_out, st, true);
+}
+
+// pipelined: returns once the step is enqueued; *loss_out = the previous pipelined step's
+// loss (its copy was enqueued with that step; waiting for it here cannot stall the device)
 dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                      const void* const* host_ptrs, const int64_t* ld, int64_t rows,
-                                     float* loss_out, cudaStream_t st) {
+                                     float* loss_out, cudaStream_t st, bool pipelined, int32_t* has_loss) {
   if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
   if (n_feeds < 0 || n_feeds > 2 || (n_feeds > 0 && (!feeds || !host_ptrs || !ld)))
     return fail(DFLOW_INVALID_ARGUMENT, "bad feed arrays");
@@ -1384,9 +1401,11 @@ dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_
     sids[i] = (feeds[i] >= 0 && feeds[i] < (int)s->remap.size()) ? s->remap[feeds[i]] : -1;
     if (sids[i] < 0) return fail(DFLOW_INVALID_ARGUMENT, "bad feed node");
   }
-  CU(cudaStreamWaitEvent(s->h2d, s->ev_feeds_free, 0));  // the previous forward is done with them
-  // x first, then y (its upload overlaps the first layers of the forward)
+  if (has_loss) *has_loss = 0;
+  // x first, then y (its upload overlaps the first layers of the forward); each waits for
+  // the previous step to be done with its staging buffer (x: the input cast; y: the loss GEMM)
   for (int pass = 0; pass < 2; ++pass) {
+    CU(cudaStreamWaitEvent(s->h2d, pass == 0 ? s->ev_x_free : s->ev_feeds_free, 0));
     for (int i = 0; i < n_feeds; ++i) {
       if ((sids[i] == s->y) != (pass == 1)) continue;
       const size_t esz = (sids[i] == s->x && s->x_dtype == DFLOW_BF16) ? 2 : 4;
@@ -1405,11 +1424,42 @@ dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_
   CU(cudaStreamWaitEvent(st, s->ev_h2d, 0));
   s->y_upload_pending = true;
   float loss = 0.f;
+  if (pipelined) {
+    const int prev = s->loss_slot ^ 1;
+    s->loss_slot = prev ^ 1;  // this step's loss goes to the current slot
+    const dflow_status r = session_train_step_impl(s, n_feeds, feeds, dptrs, ld, rows, &loss, st, false);
+    s->y_upload_pending = false;
+    if (r != DFLOW_OK) return r;
+    const bool had = s->loss_pending[prev];
+    ST(wait_loss(s, &loss, prev));  // the previous step's loss (its host buffers are free now too)
+    s->loss_slot = prev;            // the next pipelined step writes the other slot
+    if (had) {
+      if (loss_out) *loss_out = loss;
+      if (has_loss) *has_loss = 1;
+    }
+    return DFLOW_OK;
+  }
   const dflow_status r = session_train_step(s, n_feeds, feeds, dptrs, ld, rows, &loss, st);
   s->y_upload_pending = false;
   if (r != DFLOW_OK) return r;
   if (loss_out) *loss_out = loss;
   else CU(cudaEventSynchronize(s->ev_h2d_y));  // host_ptrs are reusable on return
+  return DFLOW_OK;
+}
+
+// The loss of the last pipelined host step (waits for it), if one is pending.
+dflow_status session_last_loss(dflow_session* s, float* loss_out, int32_t* has_loss) {
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
+  if (has_loss) *has_loss = 0;
+  for (int k = 0; k < 2; ++k) {
+    const int slot = s->loss_slot ^ 1 ^ k;  // the most recent pipelined step wrote loss_slot ^ 1
+    if (!s->loss_pending[slot]) continue;
+    float v = 0.f;
+    ST(wait_loss(s, &v, slot));
+    if (loss_out) *loss_out = v;
+    if (has_loss) *has_loss = 1;
+    return DFLOW_OK;
+  }
   return DFLOW_OK;
 }
 

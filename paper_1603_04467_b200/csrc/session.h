@@ -106,14 +106,18 @@ struct dflow_session {
   int* sched_w = nullptr;  // [2][2] tile-scheduler counters of the dW GEMMs, per side stream
   bool bwd_side = false;
   cudaEvent_t ev_loss = nullptr;
-  cudaEvent_t ev_loss_ready = nullptr;  // loss value landed in loss_host (after the forward)
-  bool loss_pending = false;
+  // loss value landed in loss_host[slot] (after the forward); two slots so a pipelined
+  // host step can enqueue step i+1 while step i's loss is still unread
+  cudaEvent_t ev_loss_ready[2] = {nullptr, nullptr};
+  bool loss_pending[2] = {false, false};
+  int loss_slot = 0;
   // e2e path: host feeds are copied on their own stream so step i+1's upload overlaps
   // step i's backward; ev_feeds_free marks the forward done reading the staging buffers
   // (x is uploaded first; y, needed only by the last layer's loss epilogue, uploads while
   // the first layers run: the step's forward waits on ev_h2d, its last GEMM on ev_h2d_y)
   cudaStream_t h2d = nullptr;
   cudaEvent_t ev_h2d = nullptr, ev_h2d_y = nullptr, ev_feeds_free = nullptr;
+  cudaEvent_t ev_x_free = nullptr;  // the input cast is done with the x staging buffer
   bool y_upload_pending = false;
   // opt.graphs: captured train steps keyed by their feed signature, replayed on gstream
   struct StepGraph {
@@ -122,6 +126,7 @@ struct dflow_session {
     int64_t ldx, ldy, rows;
     bool loss;
     bool ywait;
+    int slot;  // loss slot the captured copy writes
     cudaGraphExec_t exec;
   };
   std::vector<StepGraph> step_graphs;
@@ -166,7 +171,9 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
                                 const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st);
 dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                      const void* const* host_ptrs, const int64_t* ld, int64_t rows,
-                                     float* loss_out, cudaStream_t st);
+                                     float* loss_out, cudaStream_t st, bool pipelined = false,
+                                     int32_t* has_loss = nullptr);
+dflow_status session_last_loss(dflow_session* s, float* loss_out, int32_t* has_loss);
 dflow_status session_forward(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
                              const int64_t* ld, int64_t rows, dflow_node fetch, void* out, cudaStream_t st);
 dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_node* feeds,

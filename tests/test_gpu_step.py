@@ -201,6 +201,46 @@ def test_host_fed_steps_match_device_fed_bitwise():
         host.close()
 
 
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_pipelined_host_steps_match_device_fed_bitwise(graphs):
+    # dflow_train_step_host_pipelined: every call returns the PREVIOUS step's loss; all host
+    # buffers (distinct per step, pinned) stay untouched until the next call; the losses and
+    # the parameters must be the device-fed steps', bit for bit (with and without step graphs)
+    w = with_batch(C2, 512)
+    Ws, bs = init_params(w)
+    dev = Run(w.dims, "MSE", w.lr, rows=w.batch)
+    host = Run(w.dims, "MSE", w.lr, rows=w.batch, graphs=graphs)
+    try:
+        dev.assign(Ws, bs)
+        host.assign(Ws, bs)
+        ids, lds = D.node_array([host.mlp.x, host.mlp.y]), D.i64_array([w.dims[0], w.dims[-1]])
+        steps = 5
+        bufs = [tuple(torch.from_numpy(a).pin_memory() for a in batch(w, step=k)) for k in range(steps)]
+        want = [dev.step(_dev(X.numpy()), _dev(Y.numpy())) for X, Y in bufs]
+        got = []
+        for k, (Xh, Yh) in enumerate(bufs):
+            lh, has = C.c_float(0), C.c_int32(-1)
+            D.check(D.dflow_train_step_host_pipelined(host.s, 2, ids, D.ptr_array([Xh.data_ptr(), Yh.data_ptr()]),
+                                                      lds, w.batch, C.byref(lh), C.byref(has), stream_ptr()))
+            assert has.value == (1 if k else 0), (k, has.value)
+            if has.value:
+                got.append(lh.value)
+        lh, has = C.c_float(0), C.c_int32(-1)
+        D.check(D.dflow_session_last_loss(host.s, C.byref(lh), C.byref(has)))
+        assert has.value == 1
+        got.append(lh.value)
+        D.check(D.dflow_session_last_loss(host.s, C.byref(lh), C.byref(has)))
+        assert has.value == 0  # nothing pending any more
+        assert np.array_equal(np.float32(got).view(np.uint32), np.float32(want).view(np.uint32)), (got, want)
+        Wd, bd = dev.read()
+        Wh, bh = host.read()
+        for a, b in zip(Wd + bd, Wh + bh):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    finally:
+        dev.close()
+        host.close()
+
+
 def test_p15_non_finite_guard():
     # PAPER.md:879 (lesson 5, non-finite checks): a NaN / Inf reaching the step shows up in
     # the loss and the session's nonfinite flag; a clean step clears it
