@@ -226,6 +226,8 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
     a.p2p_shard = d.p2p_shard;
     a.p2p_rank = d.p2p_rank;
     a.p2p_world = d.p2p_world;
+    a.p2p_bulk = d.p2p_bulk;
+    if (const char* e = getenv("DFLOW_P2P_BULK")) a.p2p_bulk = atoi(e) != 0;  // A/B knob
   }
   if (d.epilogue == EPI_ASYNC_PUSH) {
     if (!d.async_master || d.p2p_world < 1 || d.p2p_world > kMaxRanks || d.p2p_shard <= 0 || d.p2p_shard % 8 ||

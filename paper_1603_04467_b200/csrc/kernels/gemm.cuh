@@ -555,10 +555,37 @@ __global__ void __launch_bounds__(256, 1)
           uint16_t* stg = stg_base + q * 32 * Cfg::STG_PITCH;
           uint32_t* srow = reinterpret_cast<uint32_t*>(stg + lane * Cfg::STG_PITCH + (c & 1) * 32);
           const uint64_t ib = static_cast<uint64_t>(gm) * args.N + gn;  // bucket position of column gn
+          // bulk-store path: the row this lane staged is read by its own bulk copy of the
+          // previous chunk pair; wait until that read is done before overwriting it
+          const bool bulk = args.p2p_bulk && (args.N % 8) == 0;
+          if (bulk && !(c & 1)) ptx::bulk_wait_read_all();
 #pragma unroll
           for (int j = 0; j < 16; ++j)
             srow[j] = round16(r[2 * j], ib + 2 * j, args.r16) | (round16(r[2 * j + 1], ib + 2 * j + 1, args.r16) << 16);
-          if (c & 1) {
+          if ((c & 1) && bulk) {
+            // each lane ships its own staged row (<= 64 codes, 128 B) with one bulk copy per
+            // owner it touches: the TMA engine carries the NVLink stores, the warp moves on
+            const int gn0 = tn * BN + (c - 1) * 32;
+            const int ncols = min(64, args.N - gn0);
+            if (row_ok && ncols > 0) {
+              ptx::fence_proxy_async_shared();
+              const uint32_t src = ptx::smem_u32(stg + lane * Cfg::STG_PITCH);
+              int64_t idx = static_cast<int64_t>(gm) * args.N + gn0;
+              int left = ncols, done = 0;
+              while (left > 0) {
+                const int owner = static_cast<int>(idx / args.p2p_shard);
+                const int64_t room = static_cast<int64_t>(owner + 1) * args.p2p_shard - idx;
+                const int n = static_cast<int>(left < room ? static_cast<int64_t>(left) : room);  // multiple of 8 (shard, N, gn0)
+                uint16_t* dst = args.p2p_recv[owner] + static_cast<int64_t>(args.p2p_rank) * args.p2p_shard +
+                                (idx - static_cast<int64_t>(owner) * args.p2p_shard);
+                ptx::bulk_store(dst, src + done * 2, n * 2);
+                idx += n;
+                done += n;
+                left -= n;
+              }
+              ptx::bulk_commit();
+            }
+          } else if (c & 1) {
             __syncwarp();
             const int gm0 = tm * (BM * CG) + cta_rank * BM + q * 32;
             const int gn0 = tn * BN + (c - 1) * 32;
@@ -839,7 +866,10 @@ __global__ void __launch_bounds__(256, 1)
       if (lane == 0 && args.loss_partials) args.loss_partials[blockIdx.x * 4 + q] = loss_acc;
     }
     // the owners read these NVLink stores after a later kernel's system-scope flag
-    if constexpr (EPI == EPI_TRUNC16_P2P) __threadfence_system();
+    if constexpr (EPI == EPI_TRUNC16_P2P) {
+      if (args.p2p_bulk) ptx::bulk_wait_all();  // this thread's bulk stores are written
+      __threadfence_system();
+    }
   }
 
   ptx::tc_fence_before();

@@ -66,6 +66,7 @@ struct GemmArgs {
   int64_t p2p_shard;
   int p2p_rank;
   int p2p_world;
+  int p2p_bulk;           // 1: each staged row goes out as bulk (TMA engine) copies, not st.global
   // EPI_TRUNC16 / EPI_TRUNC16_P2P: the 16-bit code of element (m, n) is
   // round16(bits, m*N + n, r16) — truncation, or SR16 (reading A26)
   Round16 r16;
@@ -99,6 +100,7 @@ struct GemmDesc {
   int trunc_out;                            // EPI_BIAS_RELU: truncation code instead of RNE
   int64_t p2p_shard;
   int p2p_rank, p2p_world;
+  int p2p_bulk;    // EPI_TRUNC16_P2P: ship staged rows with bulk copies (TMA engine)
   int group;       // tile-raster group (M tiles); 0 = default
   int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)

@@ -672,6 +672,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       w.p2p_shard = ly.p2p.shard;
       w.p2p_rank = s->opt.rank;
       w.p2p_world = s->opt.world;
+      w.p2p_bulk = 1;
       ST(gemm_plan(s, w, &ly.wgrad_p2p));
       ly.has_wgrad_p2p = true;
     }
