@@ -29,7 +29,8 @@ struct AsyncLayer {
   int rank, world;
 };
 
-// local W32 [in*out], b32 [out] and the bf16 operand copy wop [in, ldwb] <- the shared shards
+// local W32 [in*out] (may be NULL: not refreshed), b32 [out] and the bf16 operand copy
+// wop [in, ldwb] <- the shared shards (16-byte NVLink loads when out % 4 == 0)
 cudaError_t launch_async_pull(const AsyncLayer& a, float* W32, float* b32, __nv_bfloat16* wop, int64_t ldwb,
                               cudaStream_t s);
 // db_l (sum of the per-32-row partials, fixed order) pushed into the owners' shards:

@@ -63,7 +63,7 @@ static bool make_tmap(CUtensorMap* m, const void* base, bool f32, int64_t inner,
 template <int BN, int CG, bool TF32, bool A_MN, bool B_MN, int EPI>
 static void* kernel_ptr(int* smem) {
   auto k = &gemm_kernel<BN, CG, TF32, A_MN, B_MN, EPI>;
-  constexpr int bytes = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P>::SMEM_BYTES;
+  constexpr int bytes = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P || EPI == EPI_ASYNC_PUSH>::SMEM_BYTES;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -237,6 +237,8 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
     }
     for (int r = 0; r < d.p2p_world; ++r) a.async_master[r] = d.async_master[r];
     a.async_coded = d.async_coded;
+    a.p2p_bulk = d.p2p_bulk;
+    if (const char* e = getenv("DFLOW_P2P_BULK")) a.p2p_bulk = atoi(e) != 0;  // A/B knob
     a.p2p_shard = d.p2p_shard;
     a.p2p_rank = d.p2p_rank;
     a.p2p_world = d.p2p_world;

@@ -56,7 +56,8 @@ struct GemmCfg {
   static constexpr int SCHED_DEPTH = 4;
   static constexpr int BAR_BYTES_MAX = (2 * 8 + 4 + 2 * SCHED_DEPTH) * 8 + 16 + 4 * SCHED_DEPTH;
   // EPI_TRUNC16_P2P staging: per epilogue warp a 32-row x 64-column u16 block (row pitch
-  // 72 halves), so peer stores go out as full 128-byte row segments
+  // 72 halves), so peer stores go out as full 128-byte row segments; EPI_ASYNC_PUSH reuses
+  // it as 32 rows x 32 fp32 deltas (same 144-byte pitch) for bulk reductions
   static constexpr int STG_PITCH = 72;
   static constexpr int STG_BYTES = STG ? 4 * 32 * STG_PITCH * 2 : 0;
   // as many pipeline stages as the 227 KB opt-in shared memory holds (bf16 256x256 pair: 7,
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(256, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmA2, const __grid_constant__ CUtensorMap tmB2,
                 const GemmArgs args) {
-  using Cfg = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P>;
+  using Cfg = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P || EPI == EPI_ASYNC_PUSH>;
   constexpr int BM = Cfg::BM, BK = Cfg::BK, BN_CTA = Cfg::BN_CTA, STAGES = Cfg::STAGES;
   constexpr int A_TILE = Cfg::A_TILE, B_TILE = Cfg::B_TILE, STAGE_BYTES = Cfg::STAGE_BYTES;
   constexpr int CHUNK = Cfg::CHUNK, KMMA = Cfg::KMMA, NOPS = Cfg::NOPS;
@@ -626,7 +627,35 @@ __global__ void __launch_bounds__(256, 1)
                                    : g;
               return -__fmul_rn(args.sgd_lr, gh);
             };
-            if (full_chunk && (args.N % 4) == 0) {
+            if (full_chunk && (args.N % 8) == 0 && args.p2p_bulk) {
+              // stage this row's 32 deltas and hand them to the TMA engine as bulk fp32
+              // add-reductions into the owners' shards (split at owner boundaries, multiples
+              // of 8 elements); each element is still one atomic fp32 add at its owner
+              float* srow = reinterpret_cast<float*>(stg_base + q * 32 * Cfg::STG_PITCH + lane * Cfg::STG_PITCH);
+              ptx::bulk_wait_read_all();  // this lane's previous row has been read
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                const int64_t idx = ib + j;
+                const int owner = static_cast<int>(idx / shard);
+                *reinterpret_cast<float4*>(srow + j) =
+                    make_float4(delta(j, owner), delta(j + 1, owner), delta(j + 2, owner), delta(j + 3, owner));
+              }
+              ptx::fence_proxy_async_shared();
+              const uint32_t src = ptx::smem_u32(srow);
+              int64_t idx = ib;
+              int left = 32, done = 0;
+              while (left > 0) {
+                const int owner = static_cast<int>(idx / shard);
+                const int64_t room = static_cast<int64_t>(owner + 1) * shard - idx;
+                const int n = static_cast<int>(left < room ? static_cast<int64_t>(left) : room);
+                ptx::bulk_reduce_add_f32(args.async_master[owner] + (idx - static_cast<int64_t>(owner) * shard),
+                                         src + done * 4, n * 4);
+                idx += n;
+                done += n;
+                left -= n;
+              }
+              ptx::bulk_commit();
+            } else if (full_chunk && (args.N % 4) == 0) {
               // 4 consecutive elements share an owner (shard % 8 == 0, ib % 4 == 0): one v4 reduction
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
@@ -866,9 +895,9 @@ __global__ void __launch_bounds__(256, 1)
       if (lane == 0 && args.loss_partials) args.loss_partials[blockIdx.x * 4 + q] = loss_acc;
     }
     // the owners read these NVLink stores after a later kernel's system-scope flag
-    if constexpr (EPI == EPI_TRUNC16_P2P) {
-      if (args.p2p_bulk) ptx::bulk_wait_all();  // this thread's bulk stores are written
-      __threadfence_system();
+    if constexpr (EPI == EPI_TRUNC16_P2P || EPI == EPI_ASYNC_PUSH) {
+      if (args.p2p_bulk) ptx::bulk_wait_all();  // this thread's bulk stores / reductions are done
+      if constexpr (EPI == EPI_TRUNC16_P2P) __threadfence_system();
     }
   }
 

@@ -539,6 +539,26 @@ dflow_status setup_async(dflow_session* s) {
   return DFLOW_OK;
 }
 
+// The train step's pull (async_dp = 1): layer l's shards are pulled on a side stream while
+// the forward of the earlier layers runs; the forward of layer l waits for its own pull
+// (ev_apply[l], joined like a deferred update).  The fp32 W copy is not refreshed here
+// (dflow_variable_read pulls it).
+dflow_status async_pull_pipelined(dflow_session* s, cudaStream_t st) {
+  CU(cudaEventRecord(s->ev_side_join[0], st));  // the previous step is done with the operands
+  CU(cudaStreamWaitEvent(s->side[0], s->ev_side_join[0], 0));
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    const int t = tbegin(s, 1, s->side[0]);
+    cudaError_t e = launch_async_pull(ly.async, nullptr, ly.b32, static_cast<__nv_bfloat16*>(ly.Wop.hi), ly.ld_wb,
+                                      s->side[0]);
+    tend(s, t, s->side[0]);
+    ST(check_launch(s, e, 1, "parameter pull"));
+    CU(cudaEventRecord(s->ev_apply[l], s->side[0]));
+  }
+  s->apply_pending = true;
+  return DFLOW_OK;
+}
+
 dflow_status async_pull(dflow_session* s, cudaStream_t st) {
   for (Layer& ly : s->layers) {
     const int t = tbegin(s, 1, st);
@@ -650,6 +670,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       wa.out_f32 = nullptr;
       wa.async_master = ly.async.master;
       wa.async_coded = u16_wire(s) ? 1 : 0;
+      wa.p2p_bulk = 1;  // bulk fp32 add-reductions through the TMA engine
       wa.p2p_shard = ly.shard;
       wa.p2p_rank = s->opt.rank;
       wa.p2p_world = s->opt.world;
@@ -1307,7 +1328,7 @@ dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_
   // one step's work on `stream` (also what a step graph captures)
   auto body = [&](cudaStream_t stream) -> dflow_status {
     s->launches = s->gemm_launches = 0;
-    if (s->async && s->opt.async_dp == 1) ST(async_pull(s, stream));  // the replica reads the shared parameters
+    if (s->async && s->opt.async_dp == 1) ST(async_pull_pipelined(s, stream));  // the replica reads the shared parameters
     if (s->mp) {  // f4: this rank's layers of the one replica
       ST(run_forward_mp(s, f, rows, stream));
       CU(record_event(s, s->ev_x_free, stream));
