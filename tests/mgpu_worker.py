@@ -32,7 +32,10 @@ import synth  # noqa: E402
 def main(out_path, exchange):
     p2p = 0
     defer = 0
+    host = 0
     precision = "bf16"
+    if exchange.endswith("_HOST"):  # + pipelined host-fed steps == device-fed steps, bitwise
+        exchange, host = exchange[:-5], 1
     if exchange.endswith("_DEFER"):  # options.defer_apply: the same bits as the eager join
         exchange, defer = exchange[:-6], 1
     if exchange.endswith("_TF32"):  # the fp32-faithful 3xTF32 path over the same channel
@@ -161,6 +164,49 @@ def main(out_path, exchange):
         verdict["defer_equals_eager"] = all(bool(np.array_equal(a.view(np.uint32), c.view(np.uint32)))
                                             for a, c in zip(We + be, Wg + bg))
         eager.close()
+    if host:
+        # dflow_train_step_host_pipelined (each call returns the previous step's loss, loss
+        # all-reduced on the exchange stream into alternating slots) against device-fed steps
+        # of a twin session: every loss and the final parameters bit for bit
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid3 = bytes(idt.cpu().numpy().tobytes())
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(D.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nid4 = bytes(idt.cpu().numpy().tobytes())
+        dev = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local,
+                  nccl_id=nid3, p2p=p2p, sr_seed=seed, precision=precision, defer_apply=defer)
+        hst = Run(w.dims, "MSE", w.lr, rows=b, exchange=exchange, world=world, rank=rank, device=local,
+                  nccl_id=nid4, p2p=p2p, sr_seed=seed, precision=precision, defer_apply=defer)
+        dev.assign(Ws, bs)
+        hst.assign(Ws, bs)
+        bufs = []
+        for step in range(4):
+            Xs, Ys = synth.batch(w, step=10 + step)
+            bufs.append((torch.from_numpy(np.ascontiguousarray(Xs[rank * b:(rank + 1) * b])).pin_memory(),
+                         torch.from_numpy(np.ascontiguousarray(Ys[rank * b:(rank + 1) * b])).pin_memory()))
+        want = [dev.step(Xh.cuda(), Yh.cuda()) for Xh, Yh in bufs]
+        ids, lds = D.node_array([hst.mlp.x, hst.mlp.y]), D.i64_array([w.dims[0], w.dims[-1]])
+        got = []
+        for Xh, Yh in bufs:
+            lh, has = C.c_float(0), C.c_int32(0)
+            D.check(D.dflow_train_step_host_pipelined(hst.s, 2, ids, D.ptr_array([Xh.data_ptr(), Yh.data_ptr()]),
+                                                      lds, b, C.byref(lh), C.byref(has), stream_ptr()))
+            if has.value:
+                got.append(lh.value)
+        lh, has = C.c_float(0), C.c_int32(0)
+        D.check(D.dflow_session_last_loss(hst.s, C.byref(lh), C.byref(has)))
+        got.append(lh.value)
+        Wd, bd = dev.read()
+        Wh, bh = hst.read()
+        verdict["host_pipelined_losses_equal"] = bool(
+            len(got) == len(want) and np.array_equal(np.float32(got).view(np.uint32), np.float32(want).view(np.uint32)))
+        verdict["host_pipelined_params_equal"] = all(bool(np.array_equal(a.view(np.uint32), c.view(np.uint32)))
+                                                     for a, c in zip(Wd + bd, Wh + bh))
+        dev.close()
+        hst.close()
     if rank == 0:
         with open(out_path, "w") as f:
             json.dump(verdict, f)

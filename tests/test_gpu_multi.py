@@ -37,7 +37,7 @@ def _run(n, exchange, tmp_path):
 
 @pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "FP32", "FP32_NCCL", "SR16", "SR16_P2P",
                                       "TRUNC16_P2P_TF32", "FP32_TF32", "TRUNC16_P2P_DEFER",
-                                      "TRUNC16_DEFER"])
+                                      "TRUNC16_DEFER", "TRUNC16_P2P_DEFER_HOST"])
 def test_two_gpu_replicated_step(exchange, tmp_path):
     assert torch.cuda.is_available()
     if torch.cuda.device_count() < 2:
@@ -52,8 +52,10 @@ def test_two_gpu_replicated_step(exchange, tmp_path):
     # codec's two truncations (2^-7 each) dominate, so the bf16-level gate applies
     tol = 1e-4 if exchange == "FP32_TF32" else 2e-2
     assert v["w_after_max_err"] < tol, v
-    if exchange.endswith("_DEFER"):
+    if "_DEFER" in exchange:
         assert v["defer_equals_eager"], v
+    if exchange.endswith("_HOST"):
+        assert v["host_pipelined_losses_equal"] and v["host_pipelined_params_equal"], v
 
 
 @pytest.mark.parametrize("exchange", ["TRUNC16", "TRUNC16_P2P", "SR16_P2P", "TRUNC16_P2P_DEFER"])
