@@ -214,7 +214,8 @@ dflow_status dflow_train_step(dflow_session* s, int n_feeds, const dflow_node* f
 dflow_status dflow_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                    const void* const* host_ptrs, const int64_t* ld, int64_t local_rows,
                                    float* loss_out, void* stream);
-/* Pipelined end-to-end step: the same step, but the call returns as soon as the uploads and
+/* Pipelined end-to-end step (PAPER.md:239-254 Run with feeds, fetch = C; the feed copies are the
+ * client -> device transfers of :564-572): the same step, but the call returns as soon as the uploads and
  * the step are enqueued, so the host can enqueue step i+1 while step i runs and the PCIe link
  * stays busy (x of step i+1 uploads as soon as step i's input cast has read its staging
  * buffer, y as soon as step i's loss GEMM has).  Every step still copies its loss to the host;
@@ -256,7 +257,8 @@ typedef struct {
   double gemm_flops_per_step; /* algorithmic GEMM FLOPs of one step on this rank    */
 } dflow_stats;
 /* Orders `stream` after every update still pending on the session's exchange stream
- * (options.defer_apply); a no-op otherwise.                                     */
+ * (options.defer_apply: the ApplyGradientDescent nodes of the last step, PAPER.md:262-268,
+ * may still be running); a no-op otherwise.  Errors: DFLOW_SESSION_POISONED, DFLOW_CUDA. */
 dflow_status dflow_session_sync(dflow_session* s, void* stream);
 /* Per-kernel CUDA-event timing inside dflow_train_step (off by default). */
 dflow_status dflow_session_set_timing(dflow_session* s, int enable);
