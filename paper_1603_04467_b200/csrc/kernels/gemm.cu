@@ -206,6 +206,8 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.prefetch = 0;
   if (const char* e = getenv("DFLOW_GEMM_PREFETCH")) a.prefetch = atoi(e) >= 0 ? atoi(e) : a.prefetch;
   if (const char* e = getenv("DFLOW_GEMM_DEBUG")) a.debug = atoi(e);
+  a.evict = 1;
+  if (const char* e = getenv("DFLOW_GEMM_EVICT")) a.evict = atoi(e) != 0;  // A/B knob
   a.sgd_lr = d.sgd_lr;
   a.sched = d.sched ? d.sched : default_sched();
   if (!a.sched) {

@@ -93,6 +93,19 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Epilogue traffic that is touched once per launch (targets, masks, the stored activations /
+// gradients / weights) can go through L2 with the evict-first (streaming) policy so it does
+// not push the operand panels the next tiles reuse out of L2 (args.evict)
+template <class T>
+__device__ __forceinline__ T ld_once(const T* p, bool cs) {
+  return cs ? __ldcs(p) : __ldg(p);
+}
+template <class T>
+__device__ __forceinline__ void st_once(T* p, const T& v, bool cs) {
+  if (cs) __stcs(p, v);
+  else *p = v;
+}
+
 // tf32 round-to-nearest (ties away), returned in an fp32 container (low 13 bits 0)
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -105,7 +118,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // value, or the exact fp32 value (= big + small) in the 3xTF32 path.
 template <bool TF32>
 __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, void* lo_base, int64_t ld, int64_t gm,
-                                              int gn, int N, bool vec, bool trunc = false) {
+                                              int gn, int N, bool vec, bool trunc = false, bool cs = false) {
   const bool full = gn + 32 <= N;
   if constexpr (!TF32) {
     // bf16 operand: RNE (reading A19), or — where the tensor crosses a device (f4 channel,
@@ -117,8 +130,10 @@ __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, voi
     if (full && vec) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8)
-        *reinterpret_cast<uint4*>(o + j) = make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
-                                                      pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+        st_once(reinterpret_cast<uint4*>(o + j),
+                make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]), pack_bf16x2(v[j + 4], v[j + 5]),
+                           pack_bf16x2(v[j + 6], v[j + 7])),
+                cs);
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
@@ -136,8 +151,8 @@ __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, voi
           b[e] = tf32_rna(v[j + e]);
           s[e] = __fsub_rn(v[j + e], b[e]);
         }
-        *reinterpret_cast<float4*>(oh + j) = make_float4(b[0], b[1], b[2], b[3]);
-        *reinterpret_cast<float4*>(ol + j) = make_float4(s[0], s[1], s[2], s[3]);
+        st_once(reinterpret_cast<float4*>(oh + j), make_float4(b[0], b[1], b[2], b[3]), cs);
+        st_once(reinterpret_cast<float4*>(ol + j), make_float4(s[0], s[1], s[2], s[3]), cs);
       }
     } else {
 #pragma unroll
@@ -439,6 +454,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> registers -> global =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const bool ev = args.evict != 0;
     const uint32_t tempty_leader =
         (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0) : ptx::smem_u32(&tempty[0]);
     int acc = 0;
@@ -503,7 +519,7 @@ __global__ void __launch_bounds__(256, 1)
         if (gn + 32 <= args.N && args.vec_y) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
-            const float4 t4 = __ldg(reinterpret_cast<const float4*>(yrow + j));
+            const float4 t4 = ld_once(reinterpret_cast<const float4*>(yrow + j), ev);
             yv[j] = t4.x; yv[j + 1] = t4.y; yv[j + 2] = t4.z; yv[j + 3] = t4.w;
           }
         } else {
@@ -521,7 +537,7 @@ __global__ void __launch_bounds__(256, 1)
             if (full_chunk && args.vec_out32) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<uint4*>(o + j) = make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]);
+                st_once(reinterpret_cast<uint4*>(o + j), make_uint4(r[j], r[j + 1], r[j + 2], r[j + 3]), ev);
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j)
@@ -684,14 +700,14 @@ __global__ void __launch_bounds__(256, 1)
             if (full_chunk && args.vec_out32) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
-                const float4 w4 = *reinterpret_cast<const float4*>(w + j);
+                const float4 w4 = ld_once(reinterpret_cast<const float4*>(w + j), ev);
                 v[j] = w4.x; v[j + 1] = w4.y; v[j + 2] = w4.z; v[j + 3] = w4.w;
               }
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = __fsub_rn(v[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
 #pragma unroll
               for (int j = 0; j < 32; j += 4)
-                *reinterpret_cast<float4*>(w + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                st_once(reinterpret_cast<float4*>(w + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]), ev);
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
@@ -702,7 +718,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0);
+            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0, false, ev);
           }
         } else if constexpr (EPI == EPI_BIAS_RELU) {
           if (active) {
@@ -727,7 +743,7 @@ __global__ void __launch_bounds__(256, 1)
               if (full_chunk && args.vec_out32) {
 #pragma unroll
                 for (int j = 0; j < 32; j += 4)
-                  *reinterpret_cast<float4*>(o + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                  st_once(reinterpret_cast<float4*>(o + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]), ev);
               } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
@@ -736,7 +752,7 @@ __global__ void __launch_bounds__(256, 1)
             }
             if (args.out != nullptr)
               store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0,
-                                  args.trunc_out != 0);
+                                  args.trunc_out != 0, ev);
           }
         } else if constexpr (EPI == EPI_RELUGRAD || EPI == EPI_BIAS_RELU_LOSS) {
           // dz values as stored, 0 outside the matrix; fused db column sums.
@@ -750,7 +766,7 @@ __global__ void __launch_bounds__(256, 1)
                 if constexpr (!TF32) {
 #pragma unroll
                   for (int j = 0; j < 32; j += 8) {
-                    const uint4 mv = __ldg(reinterpret_cast<const uint4*>(mrow + j));
+                    const uint4 mv = ld_once(reinterpret_cast<const uint4*>(mrow + j), ev);
                     const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
@@ -763,7 +779,7 @@ __global__ void __launch_bounds__(256, 1)
                 } else {
 #pragma unroll
                   for (int j = 0; j < 32; j += 4) {
-                    const float4 m4 = __ldg(reinterpret_cast<const float4*>(mrow + j));
+                    const float4 m4 = ld_once(reinterpret_cast<const float4*>(mrow + j), ev);
                     v[j] = m4.x > 0.f ? u32_as_f32(r[j]) : 0.f;
                     v[j + 1] = m4.y > 0.f ? u32_as_f32(r[j + 1]) : 0.f;
                     v[j + 2] = m4.z > 0.f ? u32_as_f32(r[j + 2]) : 0.f;
@@ -812,7 +828,7 @@ __global__ void __launch_bounds__(256, 1)
                 if (full_chunk && args.vec_out32) {
 #pragma unroll
                   for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4*>(o32 + j) = make_float4(av[j], av[j + 1], av[j + 2], av[j + 3]);
+                    st_once(reinterpret_cast<float4*>(o32 + j), make_float4(av[j], av[j + 1], av[j + 2], av[j + 3]), ev);
                 } else {
 #pragma unroll
                   for (int j = 0; j < 32; ++j)
@@ -820,7 +836,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0);
+            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0, false, ev);
           }
           if (args.colsum_ws != nullptr) {
             // transpose-reduce: after 5 butterfly steps lane l holds the sum over this

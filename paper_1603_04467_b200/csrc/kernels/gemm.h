@@ -52,6 +52,8 @@ struct GemmArgs {
   int vec_bias;           // 1: 16-byte vector loads are aligned for bias
   int group_m;            // tile raster: M-tiles per group (L2 reuse of the B panels)
   int prefetch;           // k-blocks the producer's L2 prefetch runs ahead of its loads (0: off)
+  int evict;              // 1: epilogue loads / stores of once-touched data use the streaming
+                          // (evict-first) L2 policy (ld/st.global.cs)
   int debug;              // profiling only (DFLOW_GEMM_DEBUG): 1 no TMA loads, 2 no epilogue work,
                           // 4 hint-free barrier waits in the producer / MMA loop
   int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
