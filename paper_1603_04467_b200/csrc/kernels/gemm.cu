@@ -117,6 +117,18 @@ static bool aligned16(const void* p, int64_t ld, int elem) {
   return p != nullptr && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ((ld * elem) & 15) == 0;
 }
 
+// 2: 32-byte aligned (256-bit epilogue accesses), 1: 16-byte aligned, 0: scalar.
+// DFLOW_GEMM_V8=0 caps it at 1 (A/B of the 256-bit accesses).
+static int vec_width(const void* p, int64_t ld, int elem) {
+  static const int allow_v8 = [] {
+    const char* e = getenv("DFLOW_GEMM_V8");
+    return e ? atoi(e) : 1;
+  }();
+  if (!aligned16(p, ld, elem)) return 0;
+  const bool a32 = (reinterpret_cast<uintptr_t>(p) & 31) == 0 && ((ld * elem) & 31) == 0;
+  return (a32 && allow_v8) ? 2 : 1;
+}
+
 cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   g_err[0] = 0;
   if (d.M <= 0 || d.N <= 0 || d.K < 0 || d.M > (1 << 30) || d.N > (1 << 30) || d.K > (1 << 30)) {
@@ -187,9 +199,13 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.ldm = d.ldm;
   const int op_elem = tf ? 4 : 2;
   const int out_elem = (d.epilogue == EPI_TRUNC16) ? 2 : op_elem;
-  a.vec_out = aligned16(d.out, d.ldo, out_elem) && (!tf || d.epilogue == EPI_TRUNC16 || aligned16(d.out2, d.ldo, 4)) ? 1 : 0;
-  a.vec_out32 = aligned16(d.out_f32, d.ldo32, 4) ? 1 : 0;
-  a.vec_mask = aligned16(d.mask, d.ldm, op_elem) ? 1 : 0;
+  // (the 256-bit paths exist for the bf16 operand stores, the bf16 mask, the fp32 W of the
+  // SGD epilogue and the targets; elsewhere any nonzero width takes the 16-byte path)
+  a.vec_out = aligned16(d.out, d.ldo, out_elem) && (!tf || d.epilogue == EPI_TRUNC16 || aligned16(d.out2, d.ldo, 4))
+                  ? ((tf || d.epilogue == EPI_TRUNC16) ? 1 : vec_width(d.out, d.ldo, out_elem))
+                  : 0;
+  a.vec_out32 = vec_width(d.out_f32, d.ldo32, 4);
+  a.vec_mask = vec_width(d.mask, d.ldm, op_elem);
   a.y = d.y;
   a.ldy = d.ldy;
   a.loss_kind = d.loss_kind;
@@ -197,7 +213,7 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   const int64_t mn = d.M * d.N;
   a.denom_pow2 = (mn > 0 && (mn & (mn - 1)) == 0) ? 1 : 0;
   a.inv_denom = 1.0f / a.loss_denom;
-  a.vec_y = aligned16(d.y, d.ldy, 4) ? 1 : 0;
+  a.vec_y = vec_width(d.y, d.ldy, 4);
   a.vec_bias = aligned16(d.bias, 0, 4) ? 1 : 0;
   a.group_m = d.group > 0 ? d.group : 8;
   if (const char* e = getenv("DFLOW_GEMM_GROUP")) a.group_m = atoi(e) > 0 ? atoi(e) : a.group_m;

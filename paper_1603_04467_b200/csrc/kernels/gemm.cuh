@@ -106,6 +106,30 @@ __device__ __forceinline__ void st_once(T* p, const T& v, bool cs) {
   else *p = v;
 }
 
+// 256-bit (32-byte) global accesses (sm_100: LDG/STG .256). Each lane of an epilogue warp
+// owns one row, so a warp-wide access touches 32 different lines; at 32 bytes per lane the
+// L1 data path moves twice the bytes per wavefront of a 16-byte access (args.vec_* == 2).
+__device__ __forceinline__ void ld_v8(const void* p, bool cs, uint32_t* r) {
+  if (cs)
+    asm volatile("ld.global.cs.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st_v8(void* p, const uint32_t* r, bool cs) {
+  if (cs)
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                 "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+  else
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                 "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
 // tf32 round-to-nearest (ties away), returned in an fp32 container (low 13 bits 0)
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -118,7 +142,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // value, or the exact fp32 value (= big + small) in the 3xTF32 path.
 template <bool TF32>
 __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, void* lo_base, int64_t ld, int64_t gm,
-                                              int gn, int N, bool vec, bool trunc = false, bool cs = false) {
+                                              int gn, int N, int vec, bool trunc = false, bool cs = false) {
   const bool full = gn + 32 <= N;
   if constexpr (!TF32) {
     // bf16 operand: RNE (reading A19), or — where the tensor crosses a device (f4 channel,
@@ -127,7 +151,15 @@ __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, voi
     for (int j = 0; j < 32; ++j)
       v[j] = trunc ? __uint_as_float(__float_as_uint(v[j]) & 0xFFFF0000u) : __bfloat162float(__float2bfloat16_rn(v[j]));
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(hi_base) + gm * ld + gn;
-    if (full && vec) {
+    if (full && vec == 2) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 16) {
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(v[j + 2 * e], v[j + 2 * e + 1]);
+        st_v8(o + j, w, cs);
+      }
+    } else if (full && vec) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8)
         st_once(reinterpret_cast<uint4*>(o + j),
@@ -515,8 +547,16 @@ __global__ void __launch_bounds__(256, 1)
       auto load_y = [&](int c, float (&yv)[32]) {
         const int gn = tn * BN + c * 32;
         if (args.loss_kind != 0 || !row_ok || gn >= args.N) return;
+        if (args.debug & 8) {  // profiling: targets taken as 0, no loads
+#pragma unroll
+          for (int j = 0; j < 32; ++j) yv[j] = 0.f;
+          return;
+        }
         const float* yrow = args.y + static_cast<int64_t>(gm) * args.ldy + gn;
-        if (gn + 32 <= args.N && args.vec_y) {
+        if (gn + 32 <= args.N && args.vec_y == 2) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) ld_v8(yrow + j, ev, reinterpret_cast<uint32_t*>(yv + j));
+        } else if (gn + 32 <= args.N && args.vec_y) {
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 t4 = ld_once(reinterpret_cast<const float4*>(yrow + j), ev);
@@ -697,7 +737,24 @@ __global__ void __launch_bounds__(256, 1)
           if (active) {
             float* w = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
             float v[32];
-            if (full_chunk && args.vec_out32) {
+            if (full_chunk && args.vec_out32 == 2) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint32_t w8[8];
+                ld_v8(w + j, ev, w8);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[j + e] = u32_as_f32(w8[e]);
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __fsub_rn(v[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint32_t w8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) w8[e] = __float_as_uint(v[j + e]);
+                st_v8(w + j, w8, ev);
+              }
+            } else if (full_chunk && args.vec_out32) {
 #pragma unroll
               for (int j = 0; j < 32; j += 4) {
                 const float4 w4 = ld_once(reinterpret_cast<const float4*>(w + j), ev);
@@ -718,7 +775,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0, false, ev);
+            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out, false, ev);
           }
         } else if constexpr (EPI == EPI_BIAS_RELU) {
           if (active) {
@@ -751,7 +808,7 @@ __global__ void __launch_bounds__(256, 1)
               }
             }
             if (args.out != nullptr)
-              store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0,
+              store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out,
                                   args.trunc_out != 0, ev);
           }
         } else if constexpr (EPI == EPI_RELUGRAD || EPI == EPI_BIAS_RELU_LOSS) {
@@ -764,10 +821,20 @@ __global__ void __launch_bounds__(256, 1)
               const OpT* mrow = reinterpret_cast<const OpT*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
               if (full_chunk && args.vec_mask) {
                 if constexpr (!TF32) {
+                  uint32_t mw16[16];  // the 32 bf16 mask values of this chunk
+                  if (args.vec_mask == 2) {
+                    ld_v8(mrow, ev, mw16);
+                    ld_v8(mrow + 16, ev, mw16 + 8);
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 8) {
+                      const uint4 mv = ld_once(reinterpret_cast<const uint4*>(mrow + j), ev);
+                      mw16[j / 2] = mv.x; mw16[j / 2 + 1] = mv.y; mw16[j / 2 + 2] = mv.z; mw16[j / 2 + 3] = mv.w;
+                    }
+                  }
 #pragma unroll
                   for (int j = 0; j < 32; j += 8) {
-                    const uint4 mv = ld_once(reinterpret_cast<const uint4*>(mrow + j), ev);
-                    const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+                    const uint32_t* mw = mw16 + j / 2;
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                       const uint32_t h = (mw[e >> 1] >> ((e & 1) * 16)) & 0xFFFFu;
@@ -836,7 +903,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out != 0, false, ev);
+            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out, false, ev);
           }
           if (args.colsum_ws != nullptr) {
             // transpose-reduce: after 5 butterfly steps lane l holds the sum over this

@@ -55,7 +55,8 @@ struct GemmArgs {
   int evict;              // 1: epilogue loads / stores of once-touched data use the streaming
                           // (evict-first) L2 policy (ld/st.global.cs)
   int debug;              // profiling only (DFLOW_GEMM_DEBUG): 1 no TMA loads, 2 no epilogue work,
-                          // 4 hint-free barrier waits in the producer / MMA loop
+                          // 4 hint-free barrier waits in the producer / MMA loop,
+                          // 8 EPI_BIAS_RELU_LOSS targets not loaded (y = 0)
   int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
   float seed_const;       // 1 / rows (SUM seed)
   float sgd_lr;           // EPI_SGD_APPLY learning rate
