@@ -407,6 +407,14 @@ def run_gpu(args, w):
                          "traffic": traffic, "peak_source": pk["source"] + peak_note,
                          "avg_launch_ms": gemm_avg_ms, "flops_per_launch": flops_per_launch,
                          "gemm_share_of_step": st.gemm_ms / max(1e-9, st.gemm_ms + st.other_ms + st.exchange_ms),
+                         # the per-launch events run in a pass after the timed region (events around
+                         # every launch, no step graph), whose clocks can differ from the timed
+                         # region's; this is the GEMM rate if the timed step split its time in the
+                         # same shares (a lower bound: it charges inter-kernel gaps to the kernels)
+                         "achieved_at_timed_step": flops_per_launch * st.gemm_launches_per_step
+                         / max(1e-12, ms / args.steps / 1000.0 * st.gemm_ms
+                               / max(1e-9, st.gemm_ms + st.other_ms)) / 1e12 * mma_mult,
+                         "timing_pass_kernel_ms_per_step": (st.gemm_ms + st.other_ms) / max(1, st.timed_steps),
                          # device time per step by kind (CUDA events around every launch, rank 0;
                          # exchange kernels run on the comm stream, overlapping the backward)
                          "kernel_ms_per_step": {"gemm": st.gemm_ms / max(1, st.timed_steps),
