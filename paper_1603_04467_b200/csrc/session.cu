@@ -27,6 +27,15 @@ namespace dflow {
 
 namespace {
 
+// Tile-raster group (M tiles per group) of one GEMM kind: forward, dgrad or wgrad. The three
+// kinds stream different panels, so each has its own A/B knob; 0 leaves the
+// plan's default (8); DFLOW_GEMM_GROUP, when set, still overrides every kind.
+constexpr int kGroupFwd = 0, kGroupDgrad = 0, kGroupWgrad = 0;
+int raster_group(const char* env, int def) {
+  const char* e = getenv(env);
+  return (e && atoi(e) > 0) ? atoi(e) : def;
+}
+
 #define CU(expr)                                                                         \
   do {                                                                                   \
     cudaError_t e_ = (expr);                                                             \
@@ -593,6 +602,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     f.B = ly.Wop.hi; f.B2 = ly.Wop.lo; f.ldb = ly.ld_wb; f.b_mn = true;
     f.bias = ly.b32;
     f.max_ctas = max_ctas;
+    f.group = raster_group("DFLOW_GEMM_GROUP_FWD", kGroupFwd);
     if (!last) {
       f.epilogue = EPI_BIAS_RELU;
       f.out = ly.A.hi; f.out2 = ly.A.lo; f.ldo = ly.ld_out;
@@ -633,6 +643,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.mask = lp.A.hi; d.ldm = lp.ld_out;
       d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
+      d.group = raster_group("DFLOW_GEMM_GROUP_DGRAD", kGroupDgrad);
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
       if (s->mp && l == s->mp_lo) {  // f4: dA_{l-1} crosses back to rank-1 as channel codes (no mask here)
@@ -651,6 +662,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     w.epilogue = EPI_F32;
     w.out_f32 = ly.g32; w.ldo32 = ly.out;
     w.max_ctas = max_ctas;
+    w.group = raster_group("DFLOW_GEMM_GROUP_WGRAD", kGroupWgrad);
     w.sched = s->sched_w + 2 * (l % 2);  // (bwd_side: dW_l runs on side[l % 2])
     ST(gemm_plan(s, w, &ly.wgrad32));
     if (s->replicas == 1 && s->trainable) {
