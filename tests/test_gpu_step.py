@@ -298,3 +298,30 @@ def test_step_graphs_replay_bitwise():
     finally:
         plain.close()
         graph.close()
+
+
+def test_raster_group_leaves_results_bitwise(monkeypatch):
+    # The tile raster (DFLOW_GEMM_GROUP_{FWD,DGRAD,WGRAD}) only reorders which SM
+    # computes which output tile: every tile's k-walk, and the per-tile loss / db partials that
+    # are summed in tile order, are unchanged, so W, b and the loss must be bit-identical.
+    w = with_batch(C3, 2048)
+    Ws, bs = init_params(w)
+    X, Y = batch(w)
+    out = []
+    for groups in [{}, {"DFLOW_GEMM_GROUP_FWD": "2", "DFLOW_GEMM_GROUP_DGRAD": "3", "DFLOW_GEMM_GROUP_WGRAD": "5"}]:
+        for k in ("DFLOW_GEMM_GROUP_FWD", "DFLOW_GEMM_GROUP_DGRAD", "DFLOW_GEMM_GROUP_WGRAD"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in groups.items():
+            monkeypatch.setenv(k, v)
+        run = Run(w.dims, w.loss, w.lr, rows=2048)
+        try:
+            run.assign(Ws, bs)
+            loss = run.step(_dev(X), _dev(Y))
+            Wg, bg = run.read()
+            out.append((loss, Wg, bg))
+        finally:
+            run.close()
+    (l0, W0, b0), (l1, W1, b1) = out
+    assert l0 == l1
+    for a, b in zip(W0 + b0, W1 + b1):
+        assert np.array_equal(a, b)
