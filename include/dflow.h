@@ -304,6 +304,44 @@ dflow_status dflow_gemm_3xtf32(int64_t M, int64_t N, int64_t K, const float* A_h
 /* The tf32 split itself (NK13, 3xTF32 path): hi = tf32_rna(src), lo = src - hi, n elements. */
 dflow_status dflow_split_tf32(const float* src, float* hi, float* lo, size_t n, void* stream);
 
+/* ------------------------------------------- simulated world (test harness)
+ * The N-GPU replicated step (§7 :934-941; §5.5 :813-821 channel) run by N sessions
+ * ("ranks") of one process on ONE GPU, so its kernels can be checked against the oracle on a
+ * single device at any N <= 8.  Each rank is a full session (its own parameters, activations,
+ * buckets, receive areas and flags) created with the same options as on N GPUs; the fused
+ * NVLink exchange stores into the other ranks' buffers on the same device (the peer pointers
+ * of CUDA IPC become the peers' own pointers), and the NCCL collectives become host
+ * rendezvous + device copies.  One host thread per rank enqueues on the world's single
+ * stream, every cross-rank wait is rendezvoused on the host first, so the device never
+ * waits on work that is not ahead of it in the stream.  Not a transport for real training.
+ *   - The sim_* calls are synchronous (they return after the world's stream is idle).
+ *   - Sessions of a world may also be used directly (dflow_variable_assign/read,
+ *     dflow_fetch_gradients, and dflow_train_step of async_dp sessions, which issue no
+ *     collective) with the world's stream; a collective reached by fewer than N ranks
+ *     fails after DFLOW_SIM_TIMEOUT_MS (default 120 s) with DFLOW_NCCL.
+ *   - Destroy the sessions (dflow_session_destroy) before the world.                   */
+typedef struct dflow_sim_world dflow_sim_world;
+dflow_status dflow_sim_world_create(int32_t world, int32_t device, dflow_sim_world** out);
+void dflow_sim_world_destroy(dflow_sim_world* w);
+/* The world's stream (cudaStream_t as void*): pass it to direct calls on its sessions. */
+dflow_status dflow_sim_world_stream(dflow_sim_world* w, void** stream_out);
+/* Fault injection: rank `rank` (-1 = none) sends no gradient contributions in later train
+ * steps (a peer that died mid-step); the other ranks' bounded flag waits time out
+ * (DFLOW_P2P_TIMEOUT_MS) and every session of the world becomes DFLOW_SESSION_POISONED.   */
+dflow_status dflow_sim_world_drop_rank(dflow_sim_world* w, int32_t rank);
+/* Creates all world-size ranks' sessions (options as dflow_session_create; world, rank and
+ * device are taken from the world).  out: [world] sessions.                             */
+dflow_status dflow_sim_sessions_create(dflow_sim_world* w, const dflow_graph* g, const dflow_options* opt,
+                                       dflow_session** out);
+/* dflow_train_step on every rank concurrently.  dev_ptrs: [world][n_feeds] (rank-major);
+ * feeds and ld shared by all ranks; loss_out: [world] or NULL.                            */
+dflow_status dflow_sim_train_step(dflow_sim_world* w, dflow_session* const* sessions, int n_feeds,
+                                  const dflow_node* feeds, const void* const* dev_ptrs, const int64_t* ld,
+                                  int64_t local_rows, float* loss_out);
+/* dflow_exchange on every rank concurrently: grads[r], outs[r] device fp32 [n].           */
+dflow_status dflow_sim_exchange(dflow_sim_world* w, dflow_session* const* sessions, const float* const* grads,
+                                float* const* outs, size_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,14 @@ _SIGS = {
                                _i64, _i32, _p]),
     "dflow_gemm_3xtf32": (_i32, [_i64, _i64, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i32, _p, _i64, _i32, _p]),
     "dflow_split_tf32": (_i32, [_p, _p, _p, _sz, _p]),
+    "dflow_sim_world_create": (_i32, [_i32, _i32, C.POINTER(_p)]),
+    "dflow_sim_world_destroy": (None, [_p]),
+    "dflow_sim_world_stream": (_i32, [_p, C.POINTER(_p)]),
+    "dflow_sim_world_drop_rank": (_i32, [_p, _i32]),
+    "dflow_sim_sessions_create": (_i32, [_p, _p, C.POINTER(dflow_options), C.POINTER(_p)]),
+    "dflow_sim_train_step": (_i32, [_p, C.POINTER(_p), _i32, _pnode, C.POINTER(_p), _pi64, _i64,
+                                    C.POINTER(C.c_float)]),
+    "dflow_sim_exchange": (_i32, [_p, C.POINTER(_p), C.POINTER(_p), C.POINTER(_p), _sz]),
 }
 
 for _name, (_res, _args) in _SIGS.items():
@@ -248,3 +256,23 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     check(dflow_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def sim_world(world: int, device: int = 0):
+    """A simulated world of `world` ranks on one GPU (include/dflow.h, test harness)."""
+    w = _p()
+    check(dflow_sim_world_create(world, device, C.byref(w)))
+    return w
+
+
+def sim_sessions(w, mlp_or_graph, opts: dflow_options, world: int):
+    g = mlp_or_graph.graph if isinstance(mlp_or_graph, MLP) else mlp_or_graph
+    out = (_p * world)()
+    check(dflow_sim_sessions_create(w, g, C.byref(opts), out))
+    return [out[r] for r in range(world)]
+
+
+def sim_stream(w):
+    st = _p()
+    check(dflow_sim_world_stream(w, C.byref(st)))
+    return st

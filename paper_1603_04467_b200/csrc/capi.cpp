@@ -17,6 +17,7 @@
 #include "kernels/elementwise.h"
 #include "kernels/gemm.h"
 #include "session.h"
+#include "sim.h"
 
 struct dflow_graph {
   dflow::Graph g;
@@ -231,7 +232,7 @@ dflow_status dflow_session_create(const dflow_graph* g, const dflow_options* opt
                                   dflow_session** out) {
   GUARD_BEGIN
   if (!g || !opt || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
-  return dflow::session_create(g->g, *opt, nccl_id128, out);
+  return dflow::session_create(g->g, *opt, nccl_id128, nullptr, out);
   GUARD_END
 }
 
@@ -414,6 +415,7 @@ dflow_status dflow_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int
   d.bias = bias;
   d.mask = mask; d.ldm = ldm;
   d.tile = tile;
+  d.sched = dflow::gemm_stream_sched(static_cast<cudaStream_t>(stream));
   dflow::GemmPlan p;
   cudaError_t e = dflow::gemm_prepare(d, sms, &p);
   if (e != cudaSuccess) return fail(DFLOW_INVALID_ARGUMENT, "%s", dflow::gemm_last_error());
@@ -439,6 +441,7 @@ dflow_status dflow_gemm_3xtf32(int64_t M, int64_t N, int64_t K, const float* A_h
   d.epilogue = dflow::EPI_F32;
   d.out_f32 = out_f32; d.ldo32 = ldo32;
   d.tile = tile;
+  d.sched = dflow::gemm_stream_sched(static_cast<cudaStream_t>(stream));
   dflow::GemmPlan p;
   cudaError_t e = dflow::gemm_prepare(d, sms, &p);
   if (e != cudaSuccess) return fail(DFLOW_INVALID_ARGUMENT, "%s", dflow::gemm_last_error());
@@ -454,6 +457,105 @@ dflow_status dflow_split_tf32(const float* src, float* hi, float* lo, size_t n, 
                                            static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(DFLOW_CUDA, "split_tf32: %s", cudaGetErrorString(e));
   return DFLOW_OK;
+}
+
+// --------------------------------------------------------- simulated world (tests)
+dflow_status dflow_sim_world_create(int32_t world, int32_t device, dflow_sim_world** out) {
+  GUARD_BEGIN
+  if (!out) return fail(DFLOW_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || world > dflow::kMaxRanks) return fail(DFLOW_INVALID_ARGUMENT, "world must be 1..%d", dflow::kMaxRanks);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(DFLOW_CUDA, "no CUDA device available (dflow has no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev || cudaSetDevice(device) != cudaSuccess)
+    return fail(DFLOW_INVALID_ARGUMENT, "bad device ordinal %d", device);
+  dflow_sim_world* w = new dflow_sim_world();
+  w->world = world;
+  w->device = device;
+  w->slot.assign(world, nullptr);
+  if (const char* e = getenv("DFLOW_SIM_TIMEOUT_MS")) w->timeout_ms = atoll(e) > 0 ? atoll(e) : w->timeout_ms;
+  if (cudaStreamCreateWithFlags(&w->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete w;
+    return fail(DFLOW_CUDA, "stream creation failed");
+  }
+  *out = w;
+  return DFLOW_OK;
+  GUARD_END
+}
+
+void dflow_sim_world_destroy(dflow_sim_world* w) {
+  if (!w) return;
+  cudaSetDevice(w->device);
+  cudaStreamSynchronize(w->stream);
+  cudaStreamDestroy(w->stream);
+  delete w;
+}
+
+dflow_status dflow_sim_world_stream(dflow_sim_world* w, void** stream_out) {
+  if (!w || !stream_out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
+  *stream_out = w->stream;
+  return DFLOW_OK;
+}
+
+dflow_status dflow_sim_world_drop_rank(dflow_sim_world* w, int32_t rank) {
+  if (!w || rank < -1 || rank >= w->world) return fail(DFLOW_INVALID_ARGUMENT, "bad rank");
+  w->drop_rank = rank;
+  return DFLOW_OK;
+}
+
+dflow_status dflow_sim_sessions_create(dflow_sim_world* w, const dflow_graph* g, const dflow_options* opt,
+                                       dflow_session** out) {
+  GUARD_BEGIN
+  if (!w || !g || !opt || !out) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
+  for (int r = 0; r < w->world; ++r) out[r] = nullptr;
+  const dflow_status st = dflow::sim_run(w, [&](int r) {
+    dflow_options o = *opt;
+    o.world = w->world;
+    o.rank = r;
+    o.device = w->device;
+    return dflow::session_create(g->g, o, nullptr, w, &out[r]);
+  });
+  if (st != DFLOW_OK) {
+    const std::string msg = dflow_last_error();
+    for (int r = 0; r < w->world; ++r) {
+      dflow::session_destroy(out[r]);
+      out[r] = nullptr;
+    }
+    return fail(st, "%s", msg.c_str());
+  }
+  return DFLOW_OK;
+  GUARD_END
+}
+
+dflow_status dflow_sim_train_step(dflow_sim_world* w, dflow_session* const* sessions, int n_feeds,
+                                  const dflow_node* feeds, const void* const* dev_ptrs, const int64_t* ld,
+                                  int64_t local_rows, float* loss_out) {
+  GUARD_BEGIN
+  if (!w || !sessions || n_feeds < 0 || (n_feeds > 0 && (!feeds || !dev_ptrs || !ld)))
+    return fail(DFLOW_INVALID_ARGUMENT, "bad arguments");
+  for (int r = 0; r < w->world; ++r)
+    if (!sessions[r] || sessions[r]->sim != w || sessions[r]->opt.rank != r)
+      return fail(DFLOW_INVALID_ARGUMENT, "sessions[%d] is not rank %d of this world", r, r);
+  return dflow::sim_run(w, [&](int r) {
+    return dflow::session_train_step(sessions[r], n_feeds, feeds, dev_ptrs + static_cast<size_t>(r) * n_feeds, ld,
+                                     local_rows, loss_out ? loss_out + r : nullptr, w->stream);
+  });
+  GUARD_END
+}
+
+dflow_status dflow_sim_exchange(dflow_sim_world* w, dflow_session* const* sessions, const float* const* grads,
+                                float* const* outs, size_t n) {
+  GUARD_BEGIN
+  if (!w || !sessions || !grads || !outs) return fail(DFLOW_INVALID_ARGUMENT, "NULL argument");
+  for (int r = 0; r < w->world; ++r)
+    if (!sessions[r] || sessions[r]->sim != w || sessions[r]->opt.rank != r)
+      return fail(DFLOW_INVALID_ARGUMENT, "sessions[%d] is not rank %d of this world", r, r);
+  return dflow::sim_run(
+      w, [&](int r) { return dflow::session_exchange(sessions[r], grads[r], outs[r], n, w->stream); });
+  GUARD_END
 }
 
 }  // extern "C"

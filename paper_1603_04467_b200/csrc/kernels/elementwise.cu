@@ -182,12 +182,21 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
+// One block of 256 threads: thread t sums partials t, t+256, ... in order, then the 8 warps'
+// shuffle trees and the 8 warp sums in warp order — a fixed summation order for a fixed n
+// (the GEMM epilogue stores one partial per (tile, CTA, warp), so n and every slot are fixed).
 __global__ void k_loss_final(int kind, const double* __restrict__ partials, int n, int64_t rows, int64_t cols,
                              float* __restrict__ loss) {
+  __shared__ double ws[8];
   double v = 0.0;
-  for (int i = threadIdx.x; i < n; i += 32) v += partials[i];
+  for (int i = threadIdx.x; i < n; i += 256) v += partials[i];
   v = warp_sum_d(v);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
   if (threadIdx.x == 0) {
+    v = ws[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += ws[w];
     const double c = (kind == 0) ? v / (2.0 * static_cast<double>(rows) * static_cast<double>(cols))
                                  : v / static_cast<double>(rows);
     *loss = static_cast<float>(c);
@@ -290,6 +299,15 @@ __global__ void k_owner_reduce_f32(const float* __restrict__ recv, int64_t shard
     float s = recv[i];
     for (int r = 1; r < nranks; ++r) s = __fadd_rn(s, recv[r * shard + i]);
     out[i] = __fmul_rn(s, inv);
+  }
+}
+
+__global__ void k_sum_ranks_f32(RankPtrs src, int nranks, float* __restrict__ dst, size_t count) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += stride) {
+    float s = src.p[0][i];
+    for (int r = 1; r < nranks; ++r) s = __fadd_rn(s, src.p[r][i]);
+    dst[i] = s;
   }
 }
 
@@ -451,7 +469,7 @@ cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat1
 
 cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t rows, int64_t cols, float* loss,
                               cudaStream_t s) {
-  k_loss_final<<<1, 32, 0, s>>>(kind, partials, n, rows, cols, loss);
+  k_loss_final<<<1, 256, 0, s>>>(kind, partials, n, rows, cols, loss);
   return cudaGetLastError();
 }
 
@@ -481,6 +499,12 @@ cudaError_t launch_relugrad_recv(const uint16_t* code, int64_t ldc, const __nv_b
 cudaError_t launch_owner_reduce_f32(const float* recv, int64_t shard, int nranks, float* out, cudaStream_t s) {
   if (shard == 0) return cudaSuccess;
   k_owner_reduce_f32<<<blocks_for(shard), kThreads, 0, s>>>(recv, shard, nranks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sum_ranks_f32(RankPtrs src, int nranks, float* dst, size_t count, cudaStream_t s) {
+  if (count == 0) return cudaSuccess;
+  k_sum_ranks_f32<<<blocks_for(static_cast<int64_t>(count)), kThreads, 0, s>>>(src, nranks, dst, count);
   return cudaGetLastError();
 }
 

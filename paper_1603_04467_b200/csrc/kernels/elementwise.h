@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "gemm.h"
 #include "round16.h"
 
 namespace dflow {
@@ -48,6 +49,12 @@ cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float
 cudaError_t launch_owner_reduce_t16(const uint16_t* recv, int64_t shard, int nranks, uint16_t* out,
                                     cudaStream_t s, Round16 r = {0, 0}, int64_t idx_base = 0);
 cudaError_t launch_owner_reduce_f32(const float* recv, int64_t shard, int nranks, float* out, cudaStream_t s);
+// Simulated transport (comm.h): dst[k] = p[0][k] + p[1][k] + ... + p[n-1][k] (fp32, rank
+// order) over the ranks' buffers on this device (the sum of an all-reduce).
+struct RankPtrs {
+  const float* p[kMaxRanks];
+};
+cudaError_t launch_sum_ranks_f32(RankPtrs src, int nranks, float* dst, size_t count, cudaStream_t s);
 // x (1/N) in place (FP32_NCCL after an allreduce-sum).
 cudaError_t launch_scale_f32(float* x, int64_t n, float scale, cudaStream_t s);
 

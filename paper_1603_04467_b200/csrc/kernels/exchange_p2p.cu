@@ -23,13 +23,45 @@ __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// thread 0 of the block spins until flags[0..n) >= epoch, then the block proceeds
-__device__ __forceinline__ void block_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
-  if (threadIdx.x == 0) {
-    for (int r = 0; r < n; ++r)
-      while (static_cast<int32_t>(ld_acquire_sys(flags + r) - epoch) < 0) __nanosleep(64);
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One thread waits until flags[0..n) >= epoch.  The fast path is the flag load alone; only
+// while a flag is behind does it read the abort word (host memory) and the clock: another
+// wait of this session has given up -> give up at once; timeout_ns passed -> raise abort.
+__device__ __noinline__ bool wait_flags_bounded(const uint32_t* flags, int n, uint32_t epoch, uint32_t* abort,
+                                                uint64_t timeout_ns) {
+  uint64_t t0 = 0;
+  for (int r = 0; r < n; ++r) {
+    while (static_cast<int32_t>(ld_acquire_sys(flags + r) - epoch) < 0) {
+      if (abort != nullptr) {
+        if (*reinterpret_cast<volatile uint32_t*>(abort) != 0) return false;
+        const uint64_t now = globaltimer_ns();
+        if (t0 == 0) {
+          t0 = now;
+        } else if (now - t0 > timeout_ns) {
+          *reinterpret_cast<volatile uint32_t*>(abort) = 1u;  // any writer writes 1: no atomic needed
+          __threadfence_system();
+          return false;
+        }
+      }
+      __nanosleep(256);
+    }
   }
+  return true;
+}
+
+// thread 0 of the block waits for flags[0..n) >= epoch; the block proceeds (true) or gives up
+// together (false)
+__device__ __forceinline__ bool block_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint32_t* abort,
+                                                 uint64_t timeout_ns) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = wait_flags_bounded(flags, n, epoch, abort, timeout_ns) ? 1 : 0;
   __syncthreads();
+  return ok != 0;
 }
 
 // The block's peer stores are ordered before thread 0 by the CTA barrier; thread 0's
@@ -84,7 +116,8 @@ __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int
 }
 
 __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16) {
-  block_wait_flags(p.flags[p.rank], p.world, epoch);  // every rank's contribution has landed
+  // every rank's contribution has landed (or the wait timed out: no fold, no signal)
+  if (!block_wait_flags(p.flags[p.rank], p.world, epoch, p.abort, p.timeout_ns)) return;
   const float inv = 1.0f / static_cast<float>(p.world);
   const uint16_t* recv = p.recv[p.rank];
   const int64_t nv = p.shard / 8;
@@ -175,9 +208,8 @@ __global__ void k_gather_w32(const P2PLayer p) {
   }
 }
 
-__global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch) {
-  block_wait_flags(flags, n, epoch);
-  __threadfence_system();
+__global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint32_t* abort, uint64_t timeout_ns) {
+  if (block_wait_flags(flags, n, epoch, abort, timeout_ns)) __threadfence_system();
 }
 
 }  // namespace
@@ -203,8 +235,9 @@ cudaError_t launch_gather_w32(const P2PLayer& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s) {
-  k_wait_flags<<<1, 32, 0, s>>>(flags, world, epoch);
+cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, uint32_t* abort, uint64_t timeout_ns,
+                              cudaStream_t s) {
+  k_wait_flags<<<1, 32, 0, s>>>(flags, world, epoch, abort, timeout_ns);
   return cudaGetLastError();
 }
 

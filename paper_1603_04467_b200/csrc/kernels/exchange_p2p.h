@@ -11,7 +11,8 @@
 //   apply (+ wait)               : waits for all N phase-1 flags, applies expand(q_bar)
 //
 // Flags are monotonically increasing step epochs (no resets); ordering uses
-// system-scope fences and release/acquire flag accesses.
+// system-scope fences and release/acquire flag accesses.  Every wait is bounded (timeout_ns):
+// a dead or desynchronised peer ends in a poisoned session, not a hung GPU.
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -36,6 +37,11 @@ struct P2PLayer {
   uint16_t* wop[kMaxRanks];    // rank j's bf16 operand copy of W [in, ldwb]
   int64_t in, out, ldwb;
   float lr_w, lr_b;
+  // bounded waits (failures abort the step): a flag wait that has not seen
+  // its epoch after timeout_ns writes 1 to *abort (host-mapped) and its kernel returns without
+  // signalling anyone, so every peer's wait times out as well; the host poisons the session
+  uint32_t* abort;
+  uint64_t timeout_ns;
 };
 
 // db_l (sum of the per-32-row partials), coded (truncate / SR16) and stored at bucket index
@@ -48,7 +54,9 @@ cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, i
 cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStream_t s, Round16 r = {0, 0});
 // owner-apply: this rank's fp32 W <- every owner's shard (NVLink loads), for reads of W
 cudaError_t launch_gather_w32(const P2PLayer& p, cudaStream_t s);
-// Block until all `world` phase-1 flags of this rank reach `epoch` (one CTA, acquire.sys).
-cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, cudaStream_t s);
+// Block until all `world` phase-1 flags of this rank reach `epoch` (one CTA, acquire.sys), or
+// give up after timeout_ns (writing *abort).
+cudaError_t launch_wait_flags(const uint32_t* flags, int world, uint32_t epoch, uint32_t* abort, uint64_t timeout_ns,
+                              cudaStream_t s);
 
 }  // namespace dflow

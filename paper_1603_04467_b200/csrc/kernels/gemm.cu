@@ -2,7 +2,9 @@
 // encoding, tile-config choice, persistent grid sizing, cluster launch.
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -64,10 +66,15 @@ template <int BN, int CG, bool TF32, bool A_MN, bool B_MN, int EPI>
 static void* kernel_ptr(int* smem) {
   auto k = &gemm_kernel<BN, CG, TF32, A_MN, B_MN, EPI>;
   constexpr int bytes = GemmCfg<BN, CG, TF32, EPI == EPI_TRUNC16_P2P || EPI == EPI_ASYNC_PUSH>::SMEM_BYTES;
-  static bool attr_set = false;
-  if (!attr_set) {
+  // the opt-in to >48 KB of dynamic shared memory is per device: set it once per device
+  // (threads racing here both set it, which is harmless)
+  static std::atomic<uint64_t> attr_set{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(attr_set.load(std::memory_order_acquire) & bit)) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    attr_set = true;
+    attr_set.fetch_or(bit, std::memory_order_acq_rel);
   }
   *smem = bytes;
   return reinterpret_cast<void*>(k);
@@ -96,21 +103,23 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi, int* smem) {
   return nullptr;
 }
 
-// Per-device tile-scheduler counters [counter, done]; zeroed once, and every GEMM
-// launch leaves them zero again, so launches serialised on a stream can share them.
-static int* default_sched() {
-  static int* ptrs[64] = {nullptr};
+// Tile-scheduler counters [counter, done] per (device, stream); zeroed once, and every GEMM
+// launch leaves them zero again, so launches serialised on one stream can share them (and
+// GEMMs on different streams never do).  Sessions pass their own counters in GemmDesc.sched.
+int* gemm_stream_sched(cudaStream_t stream) {
+  static std::map<std::pair<int, cudaStream_t>, int*> ptrs;
   static std::mutex mu;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
   std::lock_guard<std::mutex> lock(mu);
-  if (!ptrs[dev]) {
+  int*& slot = ptrs[{dev, stream}];
+  if (!slot) {
     void* p = nullptr;
     if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
     if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-    ptrs[dev] = static_cast<int*>(p);
+    slot = static_cast<int*>(p);
   }
-  return ptrs[dev];
+  return slot;
 }
 
 static bool aligned16(const void* p, int64_t ld, int elem) {
@@ -225,7 +234,7 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   a.evict = 1;
   if (const char* e = getenv("DFLOW_GEMM_EVICT")) a.evict = atoi(e) != 0;  // A/B knob
   a.sgd_lr = d.sgd_lr;
-  a.sched = d.sched ? d.sched : default_sched();
+  a.sched = d.sched ? d.sched : gemm_stream_sched(nullptr);
   if (!a.sched) {
     snprintf(g_err, sizeof g_err, "could not allocate the tile-scheduler counters");
     return cudaErrorMemoryAllocation;

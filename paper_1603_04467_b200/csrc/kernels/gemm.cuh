@@ -971,11 +971,15 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (num_kb > 0) release_tmem();
       }
-    }
-    if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
+      if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
+        // one partial per (tile, CTA of the pair, warp): the slot depends on the tile, not on
+        // which CTA the dynamic scheduler gave it to, so k_loss_final's order is fixed
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
-      if (lane == 0 && args.loss_partials) args.loss_partials[blockIdx.x * 4 + q] = loss_acc;
+        for (int o = 16; o > 0; o >>= 1) loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+        if (lane == 0 && args.loss_partials)
+          args.loss_partials[(static_cast<int64_t>(t) * CG + cta_rank) * 4 + q] = loss_acc;
+        loss_acc = 0.0;
+      }
     }
     // the owners read these NVLink stores after a later kernel's system-scope flag
     if constexpr (EPI == EPI_TRUNC16_P2P || EPI == EPI_ASYNC_PUSH) {

@@ -60,7 +60,7 @@ struct GemmArgs {
   int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
   float seed_const;       // 1 / rows (SUM seed)
   float sgd_lr;           // EPI_SGD_APPLY learning rate
-  double* loss_partials;  // [grid * 4] per-(CTA, epilogue warp) partial sums
+  double* loss_partials;  // [tiles * CG * 4] per-(tile, CTA, epilogue warp) partial sums
   // EPI_RELUGRAD / EPI_BIAS_RELU_LOSS: column sums of the stored dz per 32-row block
   float* colsum_ws;       // [ceil(M / 32), N] or nullptr
   // EPI_TRUNC16_P2P: element (m, n) is bucket index m*N + n, owned by rank idx / p2p_shard;
@@ -107,8 +107,8 @@ struct GemmDesc {
   int group;       // tile-raster group (M tiles); 0 = default
   int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)
-  int* sched;      // tile-scheduler counters [2] (zeroed); NULL = the per-device default.
-                   // GEMMs that may run concurrently must not share counters
+  int* sched;      // tile-scheduler counters [2] (zeroed); NULL = those of the device's legacy
+                   // stream.  GEMMs that may run concurrently must not share counters
 };
 
 // Prepared launch: tensor maps + args, reusable across calls while buffers stay put.
@@ -127,6 +127,8 @@ struct GemmPlan {
 // Returns cudaSuccess or an error (cudaErrorInvalidValue for unsupported layouts).
 cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan);
 cudaError_t gemm_launch(const GemmPlan& plan, cudaStream_t stream);
+// Tile-scheduler counters owned by (current device, stream), for GEMMs outside a session.
+int* gemm_stream_sched(cudaStream_t stream);
 const char* gemm_last_error();
 
 }  // namespace dflow

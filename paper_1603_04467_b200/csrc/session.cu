@@ -22,6 +22,7 @@
 
 #include "common.h"
 #include "kernels/elementwise.h"
+#include "sim.h"
 
 namespace dflow {
 
@@ -62,6 +63,7 @@ int raster_group(const char* env, int def) {
 
 inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+dflow_status check_alive(dflow_session* s);
 int tbegin(dflow_session* s, int kind, cudaStream_t st);
 void tend(dflow_session* s, int idx, cudaStream_t st);
 dflow_status check_launch(dflow_session* s, cudaError_t e, int count, const char* what);
@@ -372,7 +374,10 @@ dflow_status alloc_state(dflow_session* s) {
   }
   s->ld_AL32 = pad_to(s->layers[s->L - 1].out, 4);
   ST(dmalloc(s, &s->AL32, cap * s->ld_AL32));
-  ST(dmalloc(s, &s->loss_partials, 4 * 1024));
+  {  // one fp64 loss partial per (tile, CTA, warp) of the last forward GEMM, either tile config
+    const int64_t outL = s->layers[s->L - 1].out;
+    ST(dmalloc(s, &s->loss_partials, ((cap + 127) / 128) * ((outL + 127) / 128) * 8));
+  }
   ST(dmalloc(s, &s->loss_dev, 4));
   s->mask_words_cap = (cap * std::max(max_out, s->layers[0].in) + 31) / 32;
   ST(dmalloc(s, &s->mask_dev, s->mask_words_cap));
@@ -382,8 +387,24 @@ dflow_status alloc_state(dflow_session* s) {
   // GEMM boundary instead of queueing behind the following persistent GEMM's CTAs
   int prio_lo = 0, prio_hi = 0;
   cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  if (cudaStreamCreateWithPriority(&s->comm, cudaStreamNonBlocking, prio_hi) != cudaSuccess)
+  if (s->sim) {  // simulated world: every rank's work goes to the world's one stream (comm.h)
+    s->comm = s->sim->stream;
+    s->comm_owned = false;
+  } else if (cudaStreamCreateWithPriority(&s->comm, cudaStreamNonBlocking, prio_hi) != cudaSuccess) {
     return fail(DFLOW_CUDA, "stream creation failed");
+  }
+  // bounded flag waits: the abort word the wait kernels write on a timeout (host-mapped, so
+  // it is read without synchronising), and the timeout (DFLOW_P2P_TIMEOUT_MS, default 60 s)
+  if (cudaHostAlloc(&s->abort_host, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess)
+    return fail(DFLOW_OOM, "cudaHostAlloc failed");
+  *s->abort_host = 0;
+  CU(cudaHostGetDevicePointer(&s->abort_dev, s->abort_host, 0));
+  {
+    const char* e = getenv("DFLOW_P2P_TIMEOUT_MS");
+    const double ms = (e && atof(e) > 0) ? atof(e) : 60000.0;
+    s->flag_timeout_ns = static_cast<uint64_t>(ms * 1e6);
+  }
+  ST(dmalloc(s, &s->sched_fd, 4));  // zeroed: forward and dgrad plans of this session
   s->ev_grad.resize(s->L);
   s->ev_apply.resize(s->L);
   for (int l = 0; l < s->L; ++l) {
@@ -435,24 +456,9 @@ dflow_status setup_p2p(dflow_session* s) {
   CU(cudaMemset(s->sym, 0, total));
   CU(cudaMalloc(&s->p2p_done, 2 * s->L * sizeof(int)));
   CU(cudaMemset(s->p2p_done, 0, 2 * s->L * sizeof(int)));
-  cudaIpcMemHandle_t h;
-  CU(cudaIpcGetMemHandle(&h, s->sym));
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  uint8_t* dev = nullptr;
-  CU(cudaMalloc(&dev, 64 * (N + 1)));
-  CU(cudaMemcpy(dev, &h, 64, cudaMemcpyHostToDevice));
-  NC(ncclAllGather(dev, dev + 64, 64, ncclUint8, s->nccl, s->comm));
-  CU(cudaStreamSynchronize(s->comm));
-  std::vector<cudaIpcMemHandle_t> all(N);
-  CU(cudaMemcpy(all.data(), dev + 64, 64 * N, cudaMemcpyDeviceToHost));
-  cudaFree(dev);
-  for (int j = 0; j < N; ++j) {
-    if (j == R) {
-      s->peer_sym[j] = s->sym;
-    } else {
-      CU(cudaIpcOpenMemHandle(&s->peer_sym[j], all[j], cudaIpcMemLazyEnablePeerAccess));
-    }
-  }
+  std::vector<void*> all;
+  ST(comm_share_ptrs(s, &s->sym, 1, &all, &s->ipc_opened));
+  for (int j = 0; j < N; ++j) s->peer_sym[j] = all[j];
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     for (int j = 0; j < N; ++j) {
@@ -465,39 +471,26 @@ dflow_status setup_p2p(dflow_session* s) {
     ly.p2p.shard = ly.shard;
     ly.p2p.rank = R;
     ly.p2p.world = N;
+    ly.p2p.abort = s->abort_dev;
+    ly.p2p.timeout_ns = s->flag_timeout_ns;
   }
   if (s->tf32) return DFLOW_OK;
   // owner-apply: every rank maps every peer's W32, b32 and bf16 W copy
-  const int per = 3 * s->L;  // handles per rank
-  std::vector<cudaIpcMemHandle_t> mine(per);
+  const int per = 3 * s->L;  // allocations per rank
+  std::vector<void*> mine(per);
   for (int l = 0; l < s->L; ++l) {
-    CU(cudaIpcGetMemHandle(&mine[3 * l], s->layers[l].W32));
-    CU(cudaIpcGetMemHandle(&mine[3 * l + 1], s->layers[l].b32));
-    CU(cudaIpcGetMemHandle(&mine[3 * l + 2], s->layers[l].Wop.hi));
+    mine[3 * l] = s->layers[l].W32;
+    mine[3 * l + 1] = s->layers[l].b32;
+    mine[3 * l + 2] = s->layers[l].Wop.hi;
   }
-  uint8_t* hd = nullptr;
-  CU(cudaMalloc(&hd, 64 * per * (N + 1)));
-  CU(cudaMemcpy(hd, mine.data(), 64 * per, cudaMemcpyHostToDevice));
-  NC(ncclAllGather(hd, hd + 64 * per, 64 * per, ncclUint8, s->nccl, s->comm));
-  CU(cudaStreamSynchronize(s->comm));
-  std::vector<cudaIpcMemHandle_t> allh(per * N);
-  CU(cudaMemcpy(allh.data(), hd + 64 * per, 64 * per * N, cudaMemcpyDeviceToHost));
-  cudaFree(hd);
+  std::vector<void*> allp;
+  ST(comm_share_ptrs(s, mine.data(), per, &allp, &s->ipc_opened));
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     for (int j = 0; j < N; ++j) {
-      void* ptrs[3];
-      for (int k = 0; k < 3; ++k) {
-        if (j == R) {
-          ptrs[k] = k == 0 ? static_cast<void*>(ly.W32) : k == 1 ? static_cast<void*>(ly.b32) : ly.Wop.hi;
-        } else {
-          CU(cudaIpcOpenMemHandle(&ptrs[k], allh[j * per + 3 * l + k], cudaIpcMemLazyEnablePeerAccess));
-          s->peer_maps.push_back(ptrs[k]);
-        }
-      }
-      ly.p2p.w32[j] = static_cast<float*>(ptrs[0]);
-      ly.p2p.b32[j] = static_cast<float*>(ptrs[1]);
-      ly.p2p.wop[j] = static_cast<uint16_t*>(ptrs[2]);
+      ly.p2p.w32[j] = static_cast<float*>(allp[j * per + 3 * l]);
+      ly.p2p.b32[j] = static_cast<float*>(allp[j * per + 3 * l + 1]);
+      ly.p2p.wop[j] = static_cast<uint16_t*>(allp[j * per + 3 * l + 2]);
     }
     ly.p2p.owner_apply = 1;
     ly.p2p.in = ly.in;
@@ -510,7 +503,7 @@ dflow_status setup_p2p(dflow_session* s) {
 }
 
 // Asynchronous replicas (f3): every rank allocates its fp32 shard of every layer bucket in
-// one symmetric allocation and maps every peer's through CUDA IPC (the same handle
+// one symmetric allocation and maps every peer's through CUDA IPC (the same pointer
 // exchange as setup_p2p).  Shards start zeroed; dflow_variable_assign publishes them.
 dflow_status setup_async(dflow_session* s) {
   const int N = s->opt.world, R = s->opt.rank;
@@ -522,20 +515,9 @@ dflow_status setup_async(dflow_session* s) {
   }
   CU(cudaMalloc(&s->sym, total));
   CU(cudaMemset(s->sym, 0, total));
-  cudaIpcMemHandle_t h;
-  CU(cudaIpcGetMemHandle(&h, s->sym));
-  uint8_t* dev = nullptr;
-  CU(cudaMalloc(&dev, 64 * (N + 1)));
-  CU(cudaMemcpy(dev, &h, 64, cudaMemcpyHostToDevice));
-  NC(ncclAllGather(dev, dev + 64, 64, ncclUint8, s->nccl, s->comm));
-  CU(cudaStreamSynchronize(s->comm));
-  std::vector<cudaIpcMemHandle_t> all(N);
-  CU(cudaMemcpy(all.data(), dev + 64, 64 * N, cudaMemcpyDeviceToHost));
-  cudaFree(dev);
-  for (int j = 0; j < N; ++j) {
-    if (j == R) s->peer_sym[j] = s->sym;
-    else CU(cudaIpcOpenMemHandle(&s->peer_sym[j], all[j], cudaIpcMemLazyEnablePeerAccess));
-  }
+  std::vector<void*> all;
+  ST(comm_share_ptrs(s, &s->sym, 1, &all, &s->ipc_opened));
+  for (int j = 0; j < N; ++j) s->peer_sym[j] = all[j];
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     for (int j = 0; j < N; ++j) ly.async.master[j] = reinterpret_cast<float*>(static_cast<char*>(s->peer_sym[j]) + off[l]);
@@ -578,6 +560,9 @@ dflow_status async_pull(dflow_session* s, cudaStream_t st) {
   return DFLOW_OK;
 }
 
+// loss partials the last forward GEMM's epilogue writes: one per (tile, CTA, epilogue warp)
+inline int loss_slots(const GemmPlan& p) { return p.tiles_m * p.tiles_n * p.cluster * 4; }
+
 dflow_status gemm_plan(dflow_session* s, const GemmDesc& d, GemmPlan* p) {
   cudaError_t e = gemm_prepare(d, s->num_sms, p);
   if (e != cudaSuccess) return fail(DFLOW_CUDA, "GEMM plan: %s", gemm_last_error());
@@ -603,6 +588,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     f.bias = ly.b32;
     f.max_ctas = max_ctas;
     f.group = raster_group("DFLOW_GEMM_GROUP_FWD", kGroupFwd);
+    f.sched = s->sched_fd;  // this session's own counters (never another session's stream)
     if (!last) {
       f.epilogue = EPI_BIAS_RELU;
       f.out = ly.A.hi; f.out2 = ly.A.lo; f.ldo = ly.ld_out;
@@ -644,6 +630,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
       d.group = raster_group("DFLOW_GEMM_GROUP_DGRAD", kGroupDgrad);
+      d.sched = s->sched_fd + 2;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
       if (s->mp && l == s->mp_lo) {  // f4: dA_{l-1} crosses back to rank-1 as channel codes (no mask here)
@@ -797,8 +784,21 @@ dflow_status resolve_feeds(dflow_session* s, int n_feeds, const dflow_node* feed
   return DFLOW_OK;
 }
 
+// Every entry point: a CUDA/NCCL error, a failed step or a timed-out cross-GPU flag wait
+// (the abort word a wait kernel wrote) poisons the session (abort and
+// restart from the last checkpoint, which here is the caller's).
+dflow_status check_alive(dflow_session* s) {
+  if (s->abort_host && *static_cast<volatile uint32_t*>(s->abort_host) != 0 && !s->poisoned) {
+    s->poisoned = true;
+    return fail(DFLOW_SESSION_POISONED,
+                "a cross-GPU flag wait timed out (a peer rank died or fell out of step); session poisoned");
+  }
+  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error or timeout");
+  return DFLOW_OK;
+}
+
 dflow_status check_rows(dflow_session* s, int64_t rows) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
+  ST(check_alive(s));
   if (rows <= 0 || rows > s->cap)
     return fail(DFLOW_INVALID_ARGUMENT, "local_rows %lld outside 1..max_local_rows=%lld", (long long)rows,
                 (long long)s->cap);
@@ -848,7 +848,7 @@ dflow_status run_forward(dflow_session* s, const Feeds& f, int64_t rows, cudaStr
     }
     ST(launch_gemm(s, p, st));
     const int t = tbegin(s, 1, st);
-    cudaError_t e2 = launch_loss_final(s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1, s->loss_partials, p.grid * 4, rows,
+    cudaError_t e2 = launch_loss_final(s->loss_kind == DFLOW_LOSS_MSE ? 0 : 1, s->loss_partials, loss_slots(p), rows,
                                        last.out, s->loss_dev, st);
     tend(s, t, st);
     ST(check_launch(s, e2, 1, "loss reduction"));
@@ -881,9 +881,14 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st, bool joine
         if (s->p2p) {
           // fused NVLink path: contributions already sit in our receive slots (pushed by the
           // peers' dW epilogues); fold, push q_bar to every rank, wait for every owner
+          // (simulated world: every rank's contributions are enqueued before any owner folds,
+          // and every owner's fold before any rank waits for the gather — comm.h)
+          ST(comm_rendezvous(s));
           ST(check_launch(s, launch_owner_reduce_p2p(ly.p2p, s->epoch, cs, own_code), 1, "owner reduce (p2p)"));
-          ST(check_launch(s, launch_wait_flags(ly.p2p.flags[s->opt.rank] + kMaxRanks, N, s->epoch, cs), 1,
-                          "gather wait (p2p)"));
+          ST(comm_rendezvous(s));
+          ST(check_launch(s, launch_wait_flags(ly.p2p.flags[s->opt.rank] + kMaxRanks, N, s->epoch, s->abort_dev,
+                                               s->flag_timeout_ns, cs),
+                          1, "gather wait (p2p)"));
           if (ly.p2p.owner_apply) {  // the owners already updated W, b here (a9 on the owner)
             tend(s, t, cs);
             CU(cudaEventRecord(s->ev_apply[l], cs));
@@ -893,26 +898,26 @@ dflow_status exchange_apply(dflow_session* s, int l, cudaStream_t st, bool joine
           g32 = nullptr;
           break;
         }
-        NC(ncclAlltoAll(ly.q16, ly.recv, ly.shard * 2, ncclUint8, s->nccl, cs));
+        ST(comm_alltoall(s, ly.q16, ly.recv, ly.shard * 2, cs));
         ST(check_launch(s, launch_owner_reduce_t16(static_cast<uint16_t*>(ly.recv), ly.shard, N,
                                                    static_cast<uint16_t*>(ly.own), cs, own_code,
                                                    static_cast<int64_t>(s->opt.rank) * ly.shard),
                         1, "owner reduce"));
-        NC(ncclAllGather(ly.own, ly.gath, ly.shard * 2, ncclUint8, s->nccl, cs));
+        ST(comm_allgather(s, ly.own, ly.gath, ly.shard * 2, cs));
         g16 = static_cast<const uint16_t*>(ly.gath);
         g32 = nullptr;
         break;
       }
       case DFLOW_EXCHANGE_FP32: {
-        NC(ncclAlltoAll(ly.g32, ly.recv, ly.shard, ncclFloat32, s->nccl, cs));
+        ST(comm_alltoall(s, ly.g32, ly.recv, ly.shard * 4, cs));
         ST(check_launch(s, launch_owner_reduce_f32(static_cast<float*>(ly.recv), ly.shard, N,
                                                    static_cast<float*>(ly.own), cs), 1, "owner reduce"));
-        NC(ncclAllGather(ly.own, ly.gath, ly.shard, ncclFloat32, s->nccl, cs));
+        ST(comm_allgather(s, ly.own, ly.gath, ly.shard * 4, cs));
         g32 = static_cast<const float*>(ly.gath);
         break;
       }
       case DFLOW_EXCHANGE_FP32_NCCL: {
-        NC(ncclAllReduce(ly.g32, ly.g32, ly.P, ncclFloat32, ncclSum, s->nccl, cs));
+        ST(comm_allreduce_f32(s, ly.g32, ly.g32, ly.P, cs));
         ST(check_launch(s, launch_scale_f32(ly.g32, ly.P, 1.0f / static_cast<float>(N), cs), 1, "scale"));
         break;
       }
@@ -986,7 +991,9 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
       CU(cudaStreamWaitEvent(s->side[l % 2], s->ev_grad[l], 0));
       wst = s->side[l % 2];
     }
-    ST(launch_gemm(s, wp, wst));
+    // (fault injection of the simulated world: a "dead" rank sends no contributions)
+    const bool dropped = p2p && comm_dropped(s);
+    if (!dropped) ST(launch_gemm(s, wp, wst));
     // db_l: the producing epilogue left per-32-row column partials; sum them in order.
     // N > 1: on the exchange stream, under the next dgrad (it only feeds the exchange)
     const bool on_comm = mode == 0 && s->replicas > 1;
@@ -1000,7 +1007,8 @@ dflow_status run_backward(dflow_session* s, int64_t rows, cudaStream_t st, int m
     const int chunks = static_cast<int>((rows + 31) / 32);
     // N = 1: W was updated by the dW epilogue; the b_l update rides on this pass too
     const bool fused_b = mode == 0 && s->replicas == 1 && ly.has_wgrad_apply;
-    cudaError_t e = p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, cst,
+    cudaError_t e = dropped ? cudaSuccess
+                  : p2p ? launch_colsum_final_p2p(ly.colsum_ws, chunks, ly.out, ly.in * ly.out, ly.p2p, s->epoch, cst,
                                                   send_code)
                         : launch_colsum_final(ly.colsum_ws, chunks, ly.out,
                                               (t16 || fused_b) ? nullptr : ly.g32 + ly.in * ly.out,
@@ -1046,7 +1054,7 @@ dflow_status run_forward_mp(dflow_session* s, const Feeds& f, int64_t rows, cuda
     ST(check_launch(s, e, 1, "input cast"));
   } else {
     const Layer& lp = s->layers[lo - 1];  // the received codes are the bf16 operand bits
-    NC(ncclRecv(lp.A.hi, static_cast<size_t>(rows * lp.ld_out) * 2, ncclUint8, R - 1, s->nccl, st));
+    ST(comm_recv(s, lp.A.hi, static_cast<size_t>(rows * lp.ld_out) * 2, R - 1, st));
   }
   for (int l = lo; l < hi; ++l) {
     Layer& ly = s->layers[l];
@@ -1066,13 +1074,13 @@ dflow_status run_forward_mp(dflow_session* s, const Feeds& f, int64_t rows, cuda
     }
     ST(launch_gemm(s, ly.fwd, st));
     const int t = tbegin(s, 1, st);
-    cudaError_t e = launch_loss_final(need_y ? 0 : 1, s->loss_partials, ly.fwd.grid * 4, rows, ly.out, s->loss_dev, st);
+    cudaError_t e = launch_loss_final(need_y ? 0 : 1, s->loss_partials, loss_slots(ly.fwd), rows, ly.out, s->loss_dev, st);
     tend(s, t, st);
     ST(check_launch(s, e, 1, "loss reduction"));
   }
   if (R + 1 < N) {
     const Layer& ll = s->layers[hi - 1];
-    NC(ncclSend(ll.A.hi, static_cast<size_t>(rows * ll.ld_out) * 2, ncclUint8, R + 1, s->nccl, st));
+    ST(comm_send(s, ll.A.hi, static_cast<size_t>(rows * ll.ld_out) * 2, R + 1, st));
   }
   s->have_forward = true;
   s->last_rows = rows;
@@ -1086,7 +1094,7 @@ dflow_status run_backward_mp(dflow_session* s, int64_t rows, cudaStream_t st) {
     if (l == hi - 1 && R + 1 < N) {
       // the received dA codes, masked by this rank's own activation (ReluGrad on the
       // channel's output) -> dZ and its per-32-row column partials
-      NC(ncclRecv(s->mp_recv, static_cast<size_t>(rows * ly.ld_out) * 2, ncclUint8, R + 1, s->nccl, st));
+      ST(comm_recv(s, s->mp_recv, static_cast<size_t>(rows * ly.ld_out) * 2, R + 1, st));
       const int t = tbegin(s, 1, st);
       cudaError_t e = launch_relugrad_recv(s->mp_recv, ly.ld_out, static_cast<const __nv_bfloat16*>(ly.A.hi), ly.ld_out,
                                            rows, ly.out, static_cast<__nv_bfloat16*>(ly.dZ.hi), ly.ld_out,
@@ -1099,7 +1107,7 @@ dflow_status run_backward_mp(dflow_session* s, int64_t rows, cudaStream_t st) {
     } else if (l > 0) {  // l == lo on rank > 0: dA_{lo-1} leaves as codes
       ST(launch_gemm(s, ly.dgrad_send, st));
       const Layer& lp = s->layers[l - 1];
-      NC(ncclSend(lp.dZ.hi, static_cast<size_t>(rows * lp.ld_out) * 2, ncclUint8, R - 1, s->nccl, st));
+      ST(comm_send(s, lp.dZ.hi, static_cast<size_t>(rows * lp.ld_out) * 2, R - 1, st));
     }
     ST(launch_gemm(s, ly.wgrad_apply, st));  // this rank's own update (no replicas: reading A6)
     const int t = tbegin(s, 1, st);
@@ -1158,7 +1166,7 @@ cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st) {
 
 dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
   if (s->mp) {  // f4: the last rank computed C; every rank reports it
-    NC(ncclBroadcast(s->loss_dev, s->loss_dev, 1, ncclFloat32, s->opt.world - 1, s->nccl, st));
+    ST(comm_broadcast_f32(s, s->loss_dev, 1, s->opt.world - 1, st));
     CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
     CU(record_event(s, s->ev_loss_ready[s->loss_slot], st));
     s->loss_pending[s->loss_slot] = true;
@@ -1167,7 +1175,7 @@ dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
   if (s->replicas > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
     CU(cudaEventRecord(s->ev_loss, st));
     CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
-    NC(ncclAllReduce(s->loss_dev, s->loss_dev + 1, 1, ncclFloat32, ncclSum, s->nccl, s->comm));
+    ST(comm_allreduce_f32(s, s->loss_dev, s->loss_dev + 1, 1, s->comm));
     CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev + 1, sizeof(float), cudaMemcpyDeviceToHost,
                        s->comm));
     CU(cudaEventRecord(s->ev_loss_ready[s->loss_slot], s->comm));
@@ -1183,6 +1191,7 @@ dflow_status wait_loss(dflow_session* s, float* loss_out, int slot) {
   if (!s->loss_pending[slot]) return DFLOW_OK;
   s->loss_pending[slot] = false;
   CU(cudaEventSynchronize(s->ev_loss_ready[slot]));
+  ST(check_alive(s));
   float v = s->loss_host[slot];
   if (s->replicas > 1 && !s->async) v /= static_cast<float>(s->opt.world);
   if (loss_out) *loss_out = v;
@@ -1202,7 +1211,7 @@ int layer_of_variable(dflow_session* s, int sid, bool* is_bias) {
 
 // ===================================================================== API
 dflow_status session_create(const Graph& user, const dflow_options& opt, const uint8_t* nccl_id,
-                            dflow_session** out) {
+                            dflow_sim_world* sim, dflow_session** out) {
   if (!out) return fail(DFLOW_INVALID_ARGUMENT, "out is NULL");
   *out = nullptr;
   if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world)
@@ -1212,8 +1221,13 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   if (opt.exchange < DFLOW_EXCHANGE_TRUNC16 || opt.exchange > DFLOW_EXCHANGE_SR16)
     return fail(DFLOW_INVALID_ARGUMENT, "unknown exchange mode");
   if (opt.max_local_rows <= 0) return fail(DFLOW_INVALID_ARGUMENT, "max_local_rows must be > 0");
-  if (opt.world > 1 && !nccl_id) return fail(DFLOW_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
+  if (opt.world > 1 && !nccl_id && !sim) return fail(DFLOW_INVALID_ARGUMENT, "world > 1 needs an NCCL unique id");
+  if (sim && (opt.world != sim->world || opt.device != sim->device))
+    return fail(DFLOW_INVALID_ARGUMENT, "a simulated rank needs the world's size and device");
+  if (opt.world > kMaxRanks && (sim || (opt.p2p && !opt.model_parallel) || opt.async_dp))
+    return fail(DFLOW_INVALID_ARGUMENT, "at most %d ranks", kMaxRanks);
   dflow_session* s = new dflow_session();
+  s->sim = sim;
   s->opt = opt;
   s->cap = opt.max_local_rows;
   s->tf32 = opt.precision == DFLOW_PRECISION_3XTF32;
@@ -1267,12 +1281,7 @@ dflow_status session_create(const Graph& user, const dflow_options& opt, const u
   if (st == DFLOW_OK) st = alloc_state(s);
   if (st == DFLOW_OK && s->mp && s->mp_hi < s->L)
     st = dmalloc(s, &s->mp_recv, s->cap * s->layers[s->mp_hi - 1].ld_out);
-  if (st == DFLOW_OK && opt.world > 1) {
-    ncclUniqueId id;
-    memcpy(&id, nccl_id, sizeof id);
-    ncclResult_t r = ncclCommInitRank(&s->nccl, opt.world, id, opt.rank);
-    if (r != ncclSuccess) st = fail(DFLOW_NCCL, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
-  }
+  if (st == DFLOW_OK) st = comm_init(s, nccl_id);
   if (st == DFLOW_OK && s->p2p) st = setup_p2p(s);
   if (st == DFLOW_OK && s->async) st = setup_async(s);
   if (st != DFLOW_OK) {
@@ -1287,12 +1296,12 @@ void session_destroy(dflow_session* s) {
   if (!s) return;
   cudaSetDevice(s->opt.device);
   cudaDeviceSynchronize();
-  for (int j = 0; j < dflow::kMaxRanks; ++j)
-    if (s->peer_sym[j] && s->peer_sym[j] != s->sym) cudaIpcCloseMemHandle(s->peer_sym[j]);
-  for (void* p : s->peer_maps) cudaIpcCloseMemHandle(p);
+  for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->sym) cudaFree(s->sym);
   if (s->p2p_done) cudaFree(s->p2p_done);
-  if (s->nccl) ncclCommDestroy(s->nccl);
+  comm_destroy(s);
+  if (s->abort_host) cudaFreeHost(s->abort_host);
+  if (s->sched_fd) cudaFree(s->sched_fd);
   for (Layer& ly : s->layers) {
     for (void* p : {(void*)ly.W32, (void*)ly.b32, (void*)ly.g32, (void*)ly.q16, ly.recv, ly.own, ly.gath,
                     (void*)ly.colsum_ws})
@@ -1323,19 +1332,31 @@ void session_destroy(dflow_session* s) {
     if (s->side[i]) cudaStreamDestroy(s->side[i]);
     if (s->ev_side_join[i]) cudaEventDestroy(s->ev_side_join[i]);
   }
-  if (s->comm) cudaStreamDestroy(s->comm);
+  if (s->comm && s->comm_owned) cudaStreamDestroy(s->comm);
   cudaGetLastError();
   delete s;
 }
 
 // wait = false (pipelined host steps): the loss copy is enqueued into slot s->loss_slot and
 // left pending; the caller collects it later with wait_loss.
+// The feeds a train step needs, checked before anything is enqueued.
+dflow_status validate_train_feeds(dflow_session* s, const Feeds& f) {
+  const bool need_x = !s->mp || s->mp_lo == 0;
+  const bool need_y = s->loss_kind == DFLOW_LOSS_MSE && (!s->mp || s->mp_hi == s->L);
+  if (need_x && !f.x) return fail(DFLOW_INVALID_ARGUMENT, "x must be fed");
+  if (need_x && f.ldx < s->layers[0].in) return fail(DFLOW_INVALID_ARGUMENT, "ld of x < its width");
+  if (need_y && !f.y) return fail(DFLOW_INVALID_ARGUMENT, "y must be fed (MSE loss)");
+  if (need_y && f.ldy < s->layers[s->L - 1].out) return fail(DFLOW_INVALID_ARGUMENT, "ld of y < its width");
+  return DFLOW_OK;
+}
+
 dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
                                      const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st, bool wait) {
   if (!s->trainable) return fail(DFLOW_UNIMPLEMENTED, "graph has no ApplyGradientDescent nodes to run");
   ST(check_rows(s, rows));
   Feeds f;
   ST(resolve_feeds(s, n_feeds, feeds, ptrs, ld, &f));
+  ST(validate_train_feeds(s, f));  // a rejected call changes nothing, not even the step counter
   s->epoch++;  // p2p exchange flags / SR16 draws of this step
   // one step's work on `stream` (also what a step graph captures)
   auto body = [&](cudaStream_t stream) -> dflow_status {
@@ -1350,7 +1371,9 @@ dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_
     } else {
       ST(run_forward(s, f, rows, stream, FWD_TRAIN));
       CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
-      if (loss_out) ST(enqueue_loss(s, stream));
+      // synchronous replicas: every rank takes part in the loss all-reduce whether or not it
+      // asked for the value (a collective must be issued by all ranks)
+      if (loss_out || (s->replicas > 1 && !s->async)) ST(enqueue_loss(s, stream));
       ST(run_backward(s, rows, stream, 0));
     }
     s->last_launches = s->launches;
@@ -1396,10 +1419,17 @@ dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_
     CU(cudaStreamWaitEvent(st, s->ev_gout, 0));
     if (loss_out) s->loss_pending[s->loss_slot] = true;
   } else {
-    ST(body(st));
+    const dflow_status r = body(st);
+    if (r != DFLOW_OK) {  // part of the step may be enqueued: the replicas are out of step
+      s->poisoned = true;
+      return r;
+    }
   }
   CU(cudaGetLastError());
-  if (wait) ST(wait_loss(s, loss_out, s->loss_slot));
+  if (wait) {
+    if (loss_out) ST(wait_loss(s, loss_out, s->loss_slot));
+    else s->loss_pending[s->loss_slot] = false;  // (the all-reduced copy lands unread)
+  }
   if (s->timing) {
     // DFLOW_TIMING_BATCH=k: read the events back every k steps only, so the timeline
     // (DFLOW_TIMELINE) shows k consecutive steps running back to back, overlaps included
@@ -1426,7 +1456,7 @@ dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node*
 dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_node* feeds,
                                      const void* const* host_ptrs, const int64_t* ld, int64_t rows,
                                      float* loss_out, cudaStream_t st, bool pipelined, int32_t* has_loss) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
+  ST(check_alive(s));
   if (n_feeds < 0 || n_feeds > 2 || (n_feeds > 0 && (!feeds || !host_ptrs || !ld)))
     return fail(DFLOW_INVALID_ARGUMENT, "bad feed arrays");
   const void* dptrs[2];
@@ -1483,7 +1513,7 @@ dflow_status session_train_step_host(dflow_session* s, int n_feeds, const dflow_
 
 // The loss of the last pipelined host step (waits for it), if one is pending.
 dflow_status session_last_loss(dflow_session* s, float* loss_out, int32_t* has_loss) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned by an earlier CUDA/NCCL error");
+  ST(check_alive(s));
   if (has_loss) *has_loss = 0;
   for (int k = 0; k < 2; ++k) {
     const int slot = s->loss_slot ^ 1 ^ k;  // the most recent pipelined step wrote loss_slot ^ 1
@@ -1560,6 +1590,7 @@ dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_
         d.B = ly.Wop.hi; d.B2 = ly.Wop.lo; d.ldb = ly.ld_wb; d.b_mn = false;
         d.epilogue = EPI_F32;
         d.out_f32 = static_cast<float*>(out[i]); d.ldo32 = ly.in;
+        d.sched = s->sched_fd + 2;
         GemmPlan p;
         ST(gemm_plan(s, d, &p));
         ST(launch_gemm(s, p, st));
@@ -1572,7 +1603,7 @@ dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_
 }
 
 dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_host) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  ST(check_alive(s));
   if (layer < 1 || layer > s->L || !bits_host) return fail(DFLOW_INVALID_ARGUMENT, "layer must be 1..L");
   if (!s->have_forward) return fail(DFLOW_NOT_INITIALIZED, "no forward pass has run yet");
   const Layer& ly = s->layers[layer - 1];
@@ -1595,7 +1626,7 @@ dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_hos
 }
 
 dflow_status session_variable_assign(dflow_session* s, dflow_node var, const void* src, int on_dev, cudaStream_t st) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  ST(check_alive(s));
   if (var < 0 || var >= (int)s->remap.size() || !src) return fail(DFLOW_INVALID_ARGUMENT, "bad variable");
   bool is_bias;
   const int l = layer_of_variable(s, s->remap[var], &is_bias);
@@ -1624,7 +1655,7 @@ dflow_status session_variable_assign(dflow_session* s, dflow_node var, const voi
 }
 
 dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, int on_dev, cudaStream_t st) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  ST(check_alive(s));
   if (var < 0 || var >= (int)s->remap.size() || !dst) return fail(DFLOW_INVALID_ARGUMENT, "bad variable");
   bool is_bias;
   const int l = layer_of_variable(s, s->remap[var], &is_bias);
@@ -1647,14 +1678,14 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
 }
 
 dflow_status session_async_pull(dflow_session* s, cudaStream_t st) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  ST(check_alive(s));
   if (!s->async) return fail(DFLOW_INVALID_ARGUMENT, "not an async_dp session");
   cudaSetDevice(s->opt.device);
   return async_pull(s, st);
 }
 
 dflow_status session_exchange(dflow_session* s, const float* grad, float* out, size_t n, cudaStream_t st) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  ST(check_alive(s));
   const int N = s->opt.world;
   cudaSetDevice(s->opt.device);
   ST(join_apply(s, st));
@@ -1695,18 +1726,18 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
   CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
   cudaStream_t cs = s->comm;
   if (w16) {
-    NC(ncclAlltoAll(send, recv, shard * 2, ncclUint8, s->nccl, cs));
+    ST(comm_alltoall(s, send, recv, shard * 2, cs));
     CU(launch_owner_reduce_t16(static_cast<uint16_t*>(recv), shard, N, static_cast<uint16_t*>(own), cs, own_code,
                                static_cast<int64_t>(s->opt.rank) * shard));
-    NC(ncclAllGather(own, gath, shard * 2, ncclUint8, s->nccl, cs));
+    ST(comm_allgather(s, own, gath, shard * 2, cs));
     CU(launch_expand16(static_cast<uint16_t*>(gath), out, n, cs));
   } else if (s->opt.exchange == DFLOW_EXCHANGE_FP32) {
-    NC(ncclAlltoAll(send, recv, shard, ncclFloat32, s->nccl, cs));
+    ST(comm_alltoall(s, send, recv, shard * 4, cs));
     CU(launch_owner_reduce_f32(static_cast<float*>(recv), shard, N, static_cast<float*>(own), cs));
-    NC(ncclAllGather(own, gath, shard, ncclFloat32, s->nccl, cs));
+    ST(comm_allgather(s, own, gath, shard * 4, cs));
     CU(cudaMemcpyAsync(out, gath, n * sizeof(float), cudaMemcpyDeviceToDevice, cs));
   } else {
-    NC(ncclAllReduce(send, gath, npad, ncclFloat32, ncclSum, s->nccl, cs));
+    ST(comm_allreduce_f32(s, static_cast<const float*>(send), static_cast<float*>(gath), npad, cs));
     CU(launch_scale_f32(static_cast<float*>(gath), npad, 1.0f / N, cs));
     CU(cudaMemcpyAsync(out, gath, n * sizeof(float), cudaMemcpyDeviceToDevice, cs));
   }
@@ -1717,7 +1748,7 @@ dflow_status session_exchange(dflow_session* s, const float* grad, float* out, s
 }
 
 dflow_status session_sync(dflow_session* s, cudaStream_t st) {
-  if (s->poisoned) return fail(DFLOW_SESSION_POISONED, "session poisoned");
+  ST(check_alive(s));
   cudaSetDevice(s->opt.device);
   return join_apply(s, st);
 }

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/dflow.h"
+#include "comm.h"
 #include "graph.h"
 #include "kernels/async_dp.h"
 #include "kernels/exchange_p2p.h"
@@ -134,6 +135,19 @@ struct dflow_session {
   cudaEvent_t ev_gin = nullptr, ev_gout = nullptr;
   bool capturing = false;
   ncclComm_t nccl = nullptr;
+  // simulated N-rank world on one GPU (comm.h; the test harness of the N-GPU path): the
+  // transport's collectives become host rendezvous + device copies; comm is the world's
+  // shared stream (not owned)
+  dflow_sim_world* sim = nullptr;
+  void* sim_scratch = nullptr;
+  size_t sim_scratch_bytes = 0;
+  bool comm_owned = true;
+  // bounded cross-GPU flag waits (exchange_p2p.h): a wait that times out writes a code here
+  // (pinned, mapped) and its kernel returns; the next call poisons the session
+  uint32_t* abort_host = nullptr;
+  uint32_t* abort_dev = nullptr;
+  uint64_t flag_timeout_ns = 0;
+  int* sched_fd = nullptr;  // [2][2] tile-scheduler counters of this session's forward / dgrad GEMMs
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;
   bool async = false;  // opt.async_dp (f3): sym holds this rank's parameter shards
@@ -144,7 +158,7 @@ struct dflow_session {
   uint16_t* mp_recv = nullptr;  // codes of dA of layer mp_hi-1 from rank+1 [cap, ld_out]
   void* sym = nullptr;
   void* peer_sym[dflow::kMaxRanks] = {};
-  std::vector<void*> peer_maps;  // owner-apply: peers' W32 / b32 / W operand copies (CUDA IPC)
+  std::vector<void*> ipc_opened;  // CUDA IPC mappings of the peers' allocations (closed at destroy)
   int* p2p_done = nullptr;
   uint32_t epoch = 0;
   bool poisoned = false;
@@ -164,8 +178,9 @@ struct dflow_session {
 };
 
 namespace dflow {
+// sim != NULL: this session is rank opt.rank of a simulated world on one GPU (comm.h)
 dflow_status session_create(const Graph& user, const dflow_options& opt, const uint8_t* nccl_id,
-                            dflow_session** out);
+                            dflow_sim_world* sim, dflow_session** out);
 void session_destroy(dflow_session* s);
 dflow_status session_train_step(dflow_session* s, int n_feeds, const dflow_node* feeds, const void* const* ptrs,
                                 const int64_t* ld, int64_t rows, float* loss_out, cudaStream_t st);
