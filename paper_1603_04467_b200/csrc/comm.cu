@@ -235,11 +235,13 @@ dflow_status comm_share_ptrs(dflow_session* s, void* const* mine, int count, std
   for (int k = 0; k < count; ++k) CU(cudaIpcGetMemHandle(&h[k], mine[k]));
   uint8_t* dev = nullptr;
   CU(cudaMalloc(&dev, 64 * count * (N + 1)));
-  CU(cudaMemcpy(dev, h.data(), 64 * count, cudaMemcpyHostToDevice));
+  // (stream-ordered copies: a plain cudaMemcpy from pageable memory may return before the
+  // data has landed, and runs on the legacy stream the non-blocking comm stream ignores)
+  CU(cudaMemcpyAsync(dev, h.data(), 64 * count, cudaMemcpyHostToDevice, s->comm));
   NC(ncclAllGather(dev, dev + 64 * count, 64 * count, ncclUint8, s->nccl, s->comm));
-  CU(cudaStreamSynchronize(s->comm));
   std::vector<cudaIpcMemHandle_t> allh(static_cast<size_t>(N) * count);
-  CU(cudaMemcpy(allh.data(), dev + 64 * count, 64 * count * N, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(allh.data(), dev + 64 * count, 64 * count * N, cudaMemcpyDeviceToHost, s->comm));
+  CU(cudaStreamSynchronize(s->comm));
   cudaFree(dev);
   for (int j = 0; j < N; ++j) {
     for (int k = 0; k < count; ++k) {

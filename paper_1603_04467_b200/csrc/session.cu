@@ -1609,6 +1609,8 @@ dflow_status session_fetch_masks(dflow_session* s, int layer, uint32_t* bits_hos
   const Layer& ly = s->layers[layer - 1];
   const int64_t rows = s->last_rows;
   const int64_t words = (rows * ly.out + 31) / 32;
+  // the forward ran on the caller's stream, which may be non-blocking: order after everything
+  CU(cudaDeviceSynchronize());
   cudaStream_t st = nullptr;
   cudaError_t e;
   if (layer == s->L)
@@ -1639,8 +1641,10 @@ dflow_status session_variable_assign(dflow_session* s, dflow_node var, const voi
   if (on_dev) {
     CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
   } else {
-    CU(cudaStreamSynchronize(st));
-    CU(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    // stream-ordered: cudaMemcpy from pageable memory may return before the DMA lands and
+    // is ordered on the legacy stream only, so a kernel on a non-blocking `st` (the weight
+    // cast below) could read stale W
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
   }
   if (!is_bias) {
     cudaError_t e = to_operand(s, ly.W32, ly.out, ly.Wop, ly.ld_wb, ly.in, ly.out, st);
@@ -1671,8 +1675,8 @@ dflow_status session_variable_read(dflow_session* s, dflow_node var, void* dst, 
   if (on_dev) {
     CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
   } else {
+    CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
-    CU(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
   }
   return DFLOW_OK;
 }

@@ -4,10 +4,14 @@ compute one by one.
 
 * forward: rows of A_1 = relu(X W_1 + b_1), recomputed in f64 from the same bf16
   operands the GPU multiplies (reading A13), within bf16 output rounding;
+* forward of every layer and the loss seed on sampled rows, by the oracle's own chain from
+  X (its activations rounded to bf16 as the path stores them, reading A13), against the
+  GPU's A_1 .. A_L and dZ_L rows — this ties the stored operands of the next check to the
+  oracle;
 * dW_L entries = sum over all 32768 rows of A_{L-1}[r, i] dZ_L[r, j], with
-  dZ_L = 1[a > 0] (a - y) / (rows * cols) rebuilt from the GPU's fp32 A_L and y and
-  rounded to bf16 as stored, recomputed in f64: the GPU's K = 32768 accumulation
-  must agree to fp32 accumulation accuracy;
+  dZ_L = 1[a > 0] (a - y) / (rows * cols) from the stored A_L and y and rounded to bf16
+  as stored, recomputed in f64: the GPU's K = 32768 accumulation must agree to fp32
+  accumulation accuracy;
 * the train step's update equals W - lr * dW element by element (reading A9).
 """
 import numpy as np
@@ -43,10 +47,23 @@ def test_c3_full_batch_sampled_parity():
         ref = np.maximum(z, 0)
         err = np.abs(A1[rs] - ref) / (np.abs(ref) + 1e-3)
         assert np.max(err) < 2 ** -7, float(np.max(err))  # bf16 rounding of the stored activation
-        del A1
+        # ---- the oracle's own forward chain on sampled rows, every layer, and the loss seed
+        A_gpu = [A1] + [run.forward(Xd, Yd, fetch=run.mlp.relus[l]) for l in range(1, w.layers)]
+        rs = g.choice(rows, 16, replace=False)
+        a = X[rs].astype(np.float64)
+        for l in range(w.layers):
+            z = OK.matmul(_bf16(a), _bf16(Ws[l]), 0, 0, "f64") + bs[l].astype(np.float64)
+            a = np.maximum(z, 0)
+            err = np.max(np.abs(A_gpu[l][rs] - a)) / np.max(np.abs(a))
+            assert err < 2e-2, (l, float(err))  # bf16 storage of every activation, propagated
+            if l + 1 < w.layers:
+                a = _bf16(a).astype(np.float64)  # stored as bf16 for the next layer (A13)
+        seed_ref = np.where(a > 0, (a - Y[rs]) / (rows * w.dims[-1]), 0.0)
+        seed_gpu = np.where(A_gpu[-1][rs] > 0, (A_gpu[-1][rs].astype(np.float64) - Y[rs]) / (rows * w.dims[-1]), 0.0)
+        assert np.max(np.abs(seed_gpu - seed_ref)) / np.max(np.abs(seed_ref)) < 2e-2
+        A3, AL = A_gpu[2], A_gpu[3]                             # bf16 values as stored (A_{L-1}), fp32 A_L
+        del A1, A_gpu
         # ---- dW_L sampled entries over the full batch (K = 32768)
-        A3 = run.forward(Xd, Yd, fetch=run.mlp.relus[2])       # bf16 values as stored (A_{L-1})
-        AL = run.forward(Xd, Yd, fetch=run.mlp.relus[3])       # fp32 A_L
         gW, gb, _ = run.gradients(Xd, Yd)
         d = (AL.astype(np.float32) - Y) / np.float32(rows * w.dims[-1])
         dZ = _bf16(np.where(AL > 0, d, 0.0).astype(np.float32)).astype(np.float64)

@@ -86,6 +86,27 @@ def test_config3_width_reduced_batch():
     assert max(errs.values()) < BF16_TOL, errs
 
 
+# SURVEY §8(c) P14, predicted before any GPU run (numpy emulation, C3 width): bf16 gradients
+# mask-locked ~5.6e-3, W after one step 7.2e-5 - 3.6e-4, loss 3e-5 - 3e-3 relative
+P14_C3_GRAD_LOCKED, P14_C3_W_AFTER = 5.6e-3, 3.6e-4
+
+
+def test_config3_width_bench_tile_configuration():
+    """C3 width at B = 2048: the auto rule picks the CTA-pair 256 x 256 kernels with the
+    dynamic tile scheduler and raster group 8 for the forward, the loss-fused forward, the
+    dgrad and the fused-SGD wgrad — the configuration bench.py times (B = 32768 only adds
+    M tiles).  Gradients mask-locked and W after one step against the oracle (A15, A22),
+    and inside a small factor of the P14 band."""
+    rows = 2048
+    errs, flips = _one_step_parity(with_batch(C3, rows))
+    print(errs, flips)
+    assert max(errs.values()) < BF16_TOL, errs
+    grad = max(v for k, v in errs.items() if k.startswith(("dW", "db")))
+    wafter = max(v for k, v in errs.items() if k.endswith("_after"))
+    assert grad < 3 * P14_C3_GRAD_LOCKED, (grad, errs)
+    assert wafter < 3 * P14_C3_W_AFTER, (wafter, errs)
+
+
 def test_p12_exact_regime_bitwise():
     # Every stored intermediate is exact in bf16 and fp32 sums are order-free:
     # the GPU step must equal the oracle bit for bit (W, b after the step and grads).
