@@ -58,9 +58,14 @@ def test_c3_full_batch_sampled_parity():
             assert err < 2e-2, (l, float(err))  # bf16 storage of every activation, propagated
             if l + 1 < w.layers:
                 a = _bf16(a).astype(np.float64)  # stored as bf16 for the next layer (A13)
+        # loss seed where both sides take the same Relu branch (a pre-activation within
+        # rounding of 0 may flip: reading A22 — counted, and required to be rare)
+        agree = (a > 0) == (A_gpu[-1][rs] > 0)
+        assert np.mean(~agree) < 1e-3, float(np.mean(~agree))
         seed_ref = np.where(a > 0, (a - Y[rs]) / (rows * w.dims[-1]), 0.0)
         seed_gpu = np.where(A_gpu[-1][rs] > 0, (A_gpu[-1][rs].astype(np.float64) - Y[rs]) / (rows * w.dims[-1]), 0.0)
-        assert np.max(np.abs(seed_gpu - seed_ref)) / np.max(np.abs(seed_ref)) < 2e-2
+        # |seed error| <= |A_L error| / (rows * cols), the A_L error bounded just above
+        assert np.max(np.abs(seed_gpu - seed_ref)[agree]) <= 2e-2 * np.max(np.abs(a)) / (rows * w.dims[-1])
         A3, AL = A_gpu[2], A_gpu[3]                             # bf16 values as stored (A_{L-1}), fp32 A_L
         del A1, A_gpu
         # ---- dW_L sampled entries over the full batch (K = 32768)
