@@ -439,6 +439,7 @@ def run_gpu(args, w):
                     "blocking_value": w.batch * e2e_steps / e2e_blocking_s,
                     "pipelined_value": w.batch * e2e_steps / e2e_pipelined_s},
             "gpu_launches": launches * args.steps,
+            "gather": ("nvlink_multicast" if st.multicast else "unicast") if world > 1 else None,
             "clocks": clk,
             "loss": {"first": first_loss.value, "last": last_loss.value},
         }

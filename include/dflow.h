@@ -255,6 +255,8 @@ typedef struct {
   double exchange_ms;        /* accumulated device time of the exchange            */
   int64_t timed_steps;
   double gemm_flops_per_step; /* algorithmic GEMM FLOPs of one step on this rank    */
+  int32_t multicast;         /* 1: the fused exchange's gather leg stores through an NVLink
+                                SHARP multicast address (one multimem.st per weight vector)  */
 } dflow_stats;
 /* Orders `stream` after every update still pending on the session's exchange stream
  * (options.defer_apply: the ApplyGradientDescent nodes of the last step, PAPER.md:262-268,

@@ -51,7 +51,8 @@ class dflow_options(C.Structure):
 class dflow_stats(C.Structure):
     _fields_ = [("launches_per_step", C.c_int32), ("gemm_launches_per_step", C.c_int32), ("layers", C.c_int32),
                 ("nonfinite", C.c_int32), ("gemm_ms", C.c_double), ("other_ms", C.c_double),
-                ("exchange_ms", C.c_double), ("timed_steps", C.c_int64), ("gemm_flops_per_step", C.c_double)]
+                ("exchange_ms", C.c_double), ("timed_steps", C.c_int64), ("gemm_flops_per_step", C.c_double),
+                ("multicast", C.c_int32)]
 
 
 _p = C.c_void_p

@@ -1,6 +1,7 @@
 // Cross-replica transport (see comm.h): NCCL, or the simulated N-rank world on one GPU.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nccl_device.h>
 
 #include <chrono>
 #include <condition_variable>
@@ -256,6 +257,60 @@ dflow_status comm_share_ptrs(dflow_session* s, void* const* mine, int count, std
     }
   }
   return DFLOW_OK;
+}
+
+struct SymRegion {
+  void* base = nullptr;
+  ncclWindow_t win = nullptr;
+  ncclDevComm dc{};
+  bool dc_ok = false;
+};
+
+namespace {
+__global__ void k_multimem_ptr(ncclWindow_t win, ncclDevComm dc, void** out) {
+  *out = ncclGetLsaMultimemPointer(win, 0, dc);
+}
+}  // namespace
+
+dflow_status comm_symmetric_alloc(dflow_session* s, size_t bytes, void** local, void** mc, SymRegion** out) {
+  *local = *mc = nullptr;
+  *out = nullptr;
+  if (s->sim || !s->nccl) return fail(DFLOW_UNIMPLEMENTED, "symmetric memory needs an NCCL communicator");
+  SymRegion* r = new SymRegion();
+  ncclResult_t e = ncclMemAlloc(&r->base, bytes);
+  if (e == ncclSuccess) e = ncclCommWindowRegister(s->nccl, r->base, bytes, &r->win, NCCL_WIN_COLL_SYMMETRIC);
+  if (e == ncclSuccess) {
+    ncclDevCommRequirements req{};
+    req.lsaMultimem = true;
+    e = ncclDevCommCreate(s->nccl, &req, &r->dc);
+    r->dc_ok = e == ncclSuccess;
+  }
+  if (e != ncclSuccess) {
+    comm_symmetric_free(s, r);
+    return fail(DFLOW_NCCL, "symmetric window: %s", ncclGetErrorString(e));
+  }
+  void** d = nullptr;
+  void* h = nullptr;
+  if (cudaMalloc(&d, sizeof(void*)) == cudaSuccess) {
+    k_multimem_ptr<<<1, 1, 0, s->comm>>>(r->win, r->dc, d);
+    if (cudaMemcpyAsync(&h, d, sizeof(void*), cudaMemcpyDeviceToHost, s->comm) != cudaSuccess ||
+        cudaStreamSynchronize(s->comm) != cudaSuccess)
+      h = nullptr;
+    cudaFree(d);
+  }
+  cudaGetLastError();
+  *local = r->base;
+  *mc = h;
+  *out = r;
+  return DFLOW_OK;
+}
+
+void comm_symmetric_free(dflow_session* s, SymRegion* r) {
+  if (!r) return;
+  if (r->dc_ok) ncclDevCommDestroy(s->nccl, &r->dc);
+  if (r->win) ncclCommWindowDeregister(s->nccl, r->win);
+  if (r->base) ncclMemFree(r->base);
+  delete r;
 }
 
 dflow_status sim_run(dflow_sim_world* w, const std::function<dflow_status(int)>& fn) {

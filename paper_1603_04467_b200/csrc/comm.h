@@ -54,6 +54,14 @@ dflow_status comm_recv(dflow_session* s, void* buf, size_t bytes, int peer, cuda
 dflow_status comm_share_ptrs(dflow_session* s, void* const* mine, int count, std::vector<void*>* all,
                              std::vector<void*>* opened);
 
+// NVLink SHARP multicast (f1, "data ... only transmitted once"): `bytes`
+// of symmetric memory on every rank (ncclMemAlloc + a symmetric NCCL window; collective) and,
+// when the switch can multicast, its multicast address: one `multimem.st` to *mc lands in every
+// rank's copy.  *mc = nullptr when multicast is unavailable (the caller keeps unicast).
+struct SymRegion;
+dflow_status comm_symmetric_alloc(dflow_session* s, size_t bytes, void** local, void** mc, SymRegion** out);
+void comm_symmetric_free(dflow_session* s, SymRegion* r);
+
 // Fault injection of the simulated world (tests of the bounded flag waits): the dropped
 // rank never sends its gradient contributions, as if it had died mid-step.
 bool comm_dropped(const dflow_session* s);

@@ -3,6 +3,7 @@
 #include <cstdint>
 
 #include "async_dp.h"
+#include "colsum.cuh"
 
 namespace dflow {
 namespace {
@@ -76,26 +77,11 @@ __global__ void k_async_publish(const AsyncLayer a, const float* __restrict__ W3
 
 __global__ void k_colsum_push(const float* __restrict__ ws, int chunks, const AsyncLayer a, float lr, int coded,
                               Round16 r16) {
-  __shared__ float sm[8][33];
-  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int64_t cols = a.out;
-  const int64_t c = blockIdx.x * 32LL + cl;
-  float t = 0.f;
-  if (c < cols) {  // the same fixed summation order as k_colsum_final
-    int k = g;
-    for (; k + 24 < chunks; k += 32) {
-      const float a0 = ws[(int64_t)k * cols + c], a1 = ws[(int64_t)(k + 8) * cols + c];
-      const float a2 = ws[(int64_t)(k + 16) * cols + c], a3 = ws[(int64_t)(k + 24) * cols + c];
-      t = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(t, a0), a1), a2), a3);
-    }
-    for (; k < chunks; k += 8) t = __fadd_rn(t, ws[(int64_t)k * cols + c]);
-  }
-  sm[g][cl] = t;
-  __syncthreads();
-  if (g == 0 && c < cols) {
-    float s = sm[0][cl];
-#pragma unroll
-    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
+  const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32 * kColsumColsPerWarp +
+                    (threadIdx.x & 7);
+  const float s = colsum_warp(ws, chunks, cols, c);  // the fixed order of colsum.cuh
+  if ((threadIdx.x & 31) < 8 && c < cols) {
     const int64_t idx = a.in * a.out + c;
     const int owner = static_cast<int>(idx / a.shard);
     const float gh = (coded && owner != a.rank) ? __uint_as_float(round16(__float_as_uint(s), idx, r16) << 16) : s;
@@ -118,7 +104,7 @@ cudaError_t launch_async_pull(const AsyncLayer& a, float* W32, float* b32, __nv_
 
 cudaError_t launch_colsum_push(const float* ws, int chunks, const AsyncLayer& a, float lr, int coded, Round16 r,
                                cudaStream_t s) {
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (a.out + 31) / 32));
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (a.out + 63) / 64));  // 8 warps x 8 columns
   k_colsum_push<<<blocks, 256, 0, s>>>(ws, chunks, a, lr, coded, r);
   return cudaGetLastError();
 }

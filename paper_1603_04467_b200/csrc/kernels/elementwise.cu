@@ -8,6 +8,7 @@
 #include <cstdint>
 
 #include "elementwise.h"
+#include "colsum.cuh"
 
 namespace dflow {
 
@@ -207,30 +208,14 @@ __global__ void k_loss_final(int kind, const double* __restrict__ partials, int 
 __device__ __forceinline__ float sgd(float w, float lr, float g) { return __fsub_rn(w, __fmul_rn(lr, g)); }
 
 // ------------------------------------------------------------------ colsum (final pass)
-// Block = 32 columns x 8 chunk-groups; group g sums chunks g, g+8, ... in order, then
-// the 8 group sums are added in group order (deterministic, ~#chunks/8 dependent adds).
+// The fixed summation order of colsum.cuh; a block of 256 threads covers 64 columns.
 __global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols, float* __restrict__ out32,
                                uint16_t* __restrict__ out16, Round16 r16, int64_t idx_base,
                                float* __restrict__ bias, float lr) {
-  __shared__ float sm[8][33];
-  const int cl = threadIdx.x & 31, g = threadIdx.x >> 5;
-  const int64_t c = blockIdx.x * 32LL + cl;
-  float t = 0.f;
-  if (c < cols) {
-    int k = g;
-    for (; k + 24 < chunks; k += 32) {  // 4 independent loads in flight, added in order
-      const float a0 = ws[(int64_t)k * cols + c], a1 = ws[(int64_t)(k + 8) * cols + c];
-      const float a2 = ws[(int64_t)(k + 16) * cols + c], a3 = ws[(int64_t)(k + 24) * cols + c];
-      t = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(t, a0), a1), a2), a3);
-    }
-    for (; k < chunks; k += 8) t = __fadd_rn(t, ws[(int64_t)k * cols + c]);
-  }
-  sm[g][cl] = t;
-  __syncthreads();
-  if (g == 0 && c < cols) {
-    float s = sm[0][cl];
-#pragma unroll
-    for (int i = 1; i < 8; ++i) s = __fadd_rn(s, sm[i][cl]);
+  const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32 * kColsumColsPerWarp +
+                    (threadIdx.x & 7);
+  const float s = colsum_warp(ws, chunks, cols, c);
+  if ((threadIdx.x & 31) < 8 && c < cols) {
     if (out32) out32[c] = s;
     if (out16) out16[c] = static_cast<uint16_t>(round16(__float_as_uint(s), idx_base + c, r16));
     if (bias) bias[c] = sgd(bias[c], lr, s);  // N = 1: ApplyGradientDescent on b_l (a9), fused
@@ -476,7 +461,7 @@ cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t r
 cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
                                 cudaStream_t s, Round16 r, int64_t idx_base, float* bias, float lr) {
   if (cols == 0) return cudaSuccess;
-  k_colsum_final<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16, r,
+  k_colsum_final<<<static_cast<unsigned>((cols + 63) / 64), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16, r,
                                                                           idx_base, bias, lr);
   return cudaGetLastError();
 }

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "colsum.cuh"
 #include "exchange_p2p.h"
 
 namespace dflow {
@@ -82,31 +83,14 @@ __device__ __forceinline__ void grid_signal(const P2PLayer& p, int phase, uint32
   }
 }
 
-// One thread per column, no shared memory (so it fits beside a running GEMM CTA on the
-// exchange stream): the same summation order as k_colsum_final — eight interleaved
-// partial sums t_g over chunks k = g, g+8, ... (left folds), then t_0 + ... + t_7 — so db
-// is bit-identical to the fetched gradient's.
+// db_l in the fixed order of colsum.cuh (no shared memory, so it fits on an SM beside a
+// resident GEMM CTA on the exchange stream): bit-identical to the fetched gradient's db.
 __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int64_t cols, int64_t base_idx,
                                    const P2PLayer p, uint32_t epoch, Round16 r16) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c < cols) {
-    float t[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) t[g] = 0.f;
-    int k0 = 0;
-    for (; k0 + 8 <= chunks; k0 += 8) {  // 8 independent loads in flight
-      float a[8];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) a[g] = ws[static_cast<int64_t>(k0 + g) * cols + c];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) t[g] = __fadd_rn(t[g], a[g]);
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-      if (k0 + g < chunks) t[g] = __fadd_rn(t[g], ws[static_cast<int64_t>(k0 + g) * cols + c]);
-    float sum = t[0];
-#pragma unroll
-    for (int g = 1; g < 8; ++g) sum = __fadd_rn(sum, t[g]);
+  const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32 * kColsumColsPerWarp +
+                    (threadIdx.x & 7);
+  const float sum = colsum_warp(ws, chunks, cols, c);
+  if ((threadIdx.x & 31) < 8 && c < cols) {
     const int64_t idx = base_idx + c;
     const int owner = static_cast<int>(idx / p.shard);
     p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
@@ -174,7 +158,14 @@ __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16
       w4[1] = make_float4(wn[4], wn[5], wn[6], wn[7]);
       const int64_t row = idx0 / p.out, col = idx0 - row * p.out;
       const uint4 hv = make_uint4(h[0], h[1], h[2], h[3]);
-      for (int j = 0; j < p.world; ++j) *reinterpret_cast<uint4*>(p.wop[j] + row * p.ldwb + col) = hv;
+      if (p.mc_wop) {  // one multicast store: the switch writes every rank's copy
+        asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(
+                         p.mc_wop + row * p.ldwb + col),
+                     "r"(hv.x), "r"(hv.y), "r"(hv.z), "r"(hv.w)
+                     : "memory");
+      } else {
+        for (int j = 0; j < p.world; ++j) *reinterpret_cast<uint4*>(p.wop[j] + row * p.ldwb + col) = hv;
+      }
     } else {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -216,7 +207,7 @@ __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint3
 
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
                                     uint32_t epoch, cudaStream_t s, Round16 r) {
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64));
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 15) / 16));  // 2 warps, 16 columns
   k_colsum_final_p2p<<<blocks, 64, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);
   return cudaGetLastError();
 }

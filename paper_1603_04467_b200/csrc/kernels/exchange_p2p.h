@@ -34,7 +34,9 @@ struct P2PLayer {
   int owner_apply;
   float* w32[kMaxRanks];       // rank j's fp32 master W [in*out] (dense, bucket order)
   float* b32[kMaxRanks];       // rank j's fp32 bias [out]
-  uint16_t* wop[kMaxRanks];    // rank j's bf16 operand copy of W [in, ldwb]
+  uint16_t* wop[kMaxRanks];    // rank j's bf16 operand copy of W [in, ldwb] (unicast pushes)
+  uint16_t* mc_wop;            // multicast address of every rank's copy (NVLink SHARP), or NULL:
+                               // one multimem.st replaces the N unicast stores of the gather leg
   int64_t in, out, ldwb;
   float lr_w, lr_b;
   // bounded waits (failures abort the step): a flag wait that has not seen

@@ -64,6 +64,7 @@ int raster_group(const char* env, int def) {
 inline int64_t pad_to(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 dflow_status check_alive(dflow_session* s);
+dflow_status setup_multicast(dflow_session* s);
 int tbegin(dflow_session* s, int kind, cudaStream_t st);
 void tend(dflow_session* s, int idx, cudaStream_t st);
 dflow_status check_launch(dflow_session* s, cudaError_t e, int count, const char* what);
@@ -475,22 +476,25 @@ dflow_status setup_p2p(dflow_session* s) {
     ly.p2p.timeout_ns = s->flag_timeout_ns;
   }
   if (s->tf32) return DFLOW_OK;
-  // owner-apply: every rank maps every peer's W32, b32 and bf16 W copy
-  const int per = 3 * s->L;  // allocations per rank
+  ST(setup_multicast(s));
+  // owner-apply: every rank maps every peer's W32, b32 and (without
+  // multicast) bf16 W copy
+  const int per = s->multicast ? 2 * s->L : 3 * s->L;  // allocations per rank
+  const int k = s->multicast ? 2 : 3;
   std::vector<void*> mine(per);
   for (int l = 0; l < s->L; ++l) {
-    mine[3 * l] = s->layers[l].W32;
-    mine[3 * l + 1] = s->layers[l].b32;
-    mine[3 * l + 2] = s->layers[l].Wop.hi;
+    mine[k * l] = s->layers[l].W32;
+    mine[k * l + 1] = s->layers[l].b32;
+    if (!s->multicast) mine[k * l + 2] = s->layers[l].Wop.hi;
   }
   std::vector<void*> allp;
   ST(comm_share_ptrs(s, mine.data(), per, &allp, &s->ipc_opened));
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     for (int j = 0; j < N; ++j) {
-      ly.p2p.w32[j] = static_cast<float*>(allp[j * per + 3 * l]);
-      ly.p2p.b32[j] = static_cast<float*>(allp[j * per + 3 * l + 1]);
-      ly.p2p.wop[j] = static_cast<uint16_t*>(allp[j * per + 3 * l + 2]);
+      ly.p2p.w32[j] = static_cast<float*>(allp[j * per + k * l]);
+      ly.p2p.b32[j] = static_cast<float*>(allp[j * per + k * l + 1]);
+      ly.p2p.wop[j] = s->multicast ? nullptr : static_cast<uint16_t*>(allp[j * per + k * l + 2]);
     }
     ly.p2p.owner_apply = 1;
     ly.p2p.in = ly.in;
@@ -498,6 +502,53 @@ dflow_status setup_p2p(dflow_session* s) {
     ly.p2p.ldwb = ly.ld_wb;
     ly.p2p.lr_w = ly.n.lr_W;
     ly.p2p.lr_b = ly.n.lr_b;
+  }
+  return DFLOW_OK;
+}
+
+// f1 multicast gather (bf16 owner-apply over NCCL): move every layer's bf16 W copy into one
+// symmetric NCCL window and store through its multicast address, so an owner writes each new
+// weight once and the NVSwitch delivers it to all N copies (instead of N unicast NVLink
+// stores).  All ranks agree (all-reduce of the outcome) or all keep unicast.
+// DFLOW_P2P_MULTICAST=0 disables it.
+dflow_status setup_multicast(dflow_session* s) {
+  if (s->sim || !s->nccl) return DFLOW_OK;
+  if (const char* e = getenv("DFLOW_P2P_MULTICAST"))
+    if (atoi(e) == 0) return DFLOW_OK;
+  size_t total = 0;
+  std::vector<size_t> off(s->L);
+  bool shapes_ok = true;
+  for (int l = 0; l < s->L; ++l) {
+    off[l] = total;
+    total += (s->layers[l].in * s->layers[l].ld_wb * 2 + 4095) / 4096 * 4096;
+    shapes_ok &= (s->layers[l].out % 8) == 0 && s->layers[l].ld_wb == s->layers[l].out;  // 16-byte rows
+  }
+  if (!shapes_ok) return DFLOW_OK;  // (the same decision on every rank: shapes are global)
+  void *base = nullptr, *mc = nullptr;
+  SymRegion* r = nullptr;
+  const dflow_status st = comm_symmetric_alloc(s, total, &base, &mc, &r);
+  // every rank must take the same path: all-reduce "this rank has a multicast address"
+  float* flag = nullptr;
+  CU(cudaMalloc(&flag, sizeof(float)));
+  const float one = (st == DFLOW_OK && mc) ? 1.f : 0.f;
+  CU(cudaMemcpyAsync(flag, &one, sizeof(float), cudaMemcpyHostToDevice, s->comm));
+  ST(comm_allreduce_f32(s, flag, flag, 1, s->comm));
+  float all = 0.f;
+  CU(cudaMemcpyAsync(&all, flag, sizeof(float), cudaMemcpyDeviceToHost, s->comm));
+  CU(cudaStreamSynchronize(s->comm));
+  cudaFree(flag);
+  if (all != static_cast<float>(s->opt.world)) {
+    if (r) comm_symmetric_free(s, r);
+    clear_error();
+    return DFLOW_OK;  // unicast pushes
+  }
+  s->wsym = r;
+  s->multicast = true;
+  for (int l = 0; l < s->L; ++l) {
+    Layer& ly = s->layers[l];
+    cudaFree(ly.Wop.hi);
+    ly.Wop.hi = static_cast<char*>(base) + off[l];
+    ly.p2p.mc_wop = reinterpret_cast<uint16_t*>(static_cast<char*>(mc) + off[l]);
   }
   return DFLOW_OK;
 }
@@ -1299,6 +1350,8 @@ void session_destroy(dflow_session* s) {
   for (void* p : s->ipc_opened) cudaIpcCloseMemHandle(p);
   if (s->sym) cudaFree(s->sym);
   if (s->p2p_done) cudaFree(s->p2p_done);
+  if (s->wsym) comm_symmetric_free(s, s->wsym);
+  s->wsym = nullptr;
   comm_destroy(s);
   if (s->abort_host) cudaFreeHost(s->abort_host);
   if (s->sched_fd) cudaFree(s->sched_fd);
@@ -1306,7 +1359,7 @@ void session_destroy(dflow_session* s) {
     for (void* p : {(void*)ly.W32, (void*)ly.b32, (void*)ly.g32, (void*)ly.q16, ly.recv, ly.own, ly.gath,
                     (void*)ly.colsum_ws})
       if (p) cudaFree(p);
-    free_operand(ly.Wop);
+    if (!s->multicast) free_operand(ly.Wop);  // (multicast: the window region, freed below)
     free_operand(ly.A);
     free_operand(ly.dZ);
   }
@@ -1775,6 +1828,7 @@ dflow_status session_stats(dflow_session* s, dflow_stats* out) {
     f += 2.0 * b * io * (l > 0 ? 3 : 2);
   }
   out->gemm_flops_per_step = f;
+  out->multicast = s->multicast ? 1 : 0;
   return DFLOW_OK;
 }
 

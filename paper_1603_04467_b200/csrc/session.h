@@ -148,6 +148,10 @@ struct dflow_session {
   uint32_t* abort_dev = nullptr;
   uint64_t flag_timeout_ns = 0;
   int* sched_fd = nullptr;  // [2][2] tile-scheduler counters of this session's forward / dgrad GEMMs
+  // f1 multicast (bf16 owner-apply over NCCL): every layer's bf16 W copy lives in one symmetric
+  // NCCL window whose multicast address the owner fold stores through (comm.h)
+  dflow::SymRegion* wsym = nullptr;
+  bool multicast = false;
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;
   bool async = false;  // opt.async_dp (f3): sym holds this rank's parameter shards
