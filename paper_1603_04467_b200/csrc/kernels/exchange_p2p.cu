@@ -207,8 +207,9 @@ __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint3
 
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
                                     uint32_t epoch, cudaStream_t s, Round16 r) {
-  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 15) / 16));  // 2 warps, 16 columns
-  k_colsum_final_p2p<<<blocks, 64, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);
+  // 8 warps x 8 columns per block: few blocks, so few system-scope fences in grid_signal
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64));
+  k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);
   return cudaGetLastError();
 }
 
