@@ -50,10 +50,18 @@ static bool make_tmap(CUtensorMap* m, const void* base, bool f32, int64_t inner,
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * e)};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t es[2] = {1, 1};
+  // L2 promotion of the operand loads (DFLOW_GEMM_L2PROMO = 0 / 64 / 128 / 256 bytes; A/B knob)
+  static const CUtensorMapL2promotion promo = [] {
+    const char* e = getenv("DFLOW_GEMM_L2PROMO");
+    const int v = e ? atoi(e) : 256;
+    return v == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                  : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                            : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }();
   CUresult r = fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
                   const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     snprintf(g_err, sizeof g_err, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%u,%u",
              (int)r, (long long)inner, (long long)outer, (long long)ld, box_inner, box_outer);
