@@ -1,7 +1,6 @@
 # 4 GPUs: N=4 parity suites; C3 N=4 and the 8-GPU proxy (N=4 at the N=8 per-GPU batch),
 # multicast gather on / off, interleaved
 set -x
-timeout 600 python -m pytest tests/test_gpu_sim_sr16.py -q -rf -s --timeout 500 > gpurun_out/r2_sr16_test.log 2>&1; tail -6 gpurun_out/r2_sr16_test.log
 timeout 1500 python -m pytest tests/test_gpu_multi.py tests/test_gpu_async.py tests/test_gpu_mp.py -q -rf --timeout 600 -k "four or 4" > gpurun_out/r2_multi4_tests.log 2>&1
 tail -4 gpurun_out/r2_multi4_tests.log
 run() {  # $1 tag, $2 multicast, extra args

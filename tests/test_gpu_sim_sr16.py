@@ -33,7 +33,7 @@ def _per_rank_grads(w, Ws, bs):
         for r in range(N):
             gW, _ = run.gradients(r, torch.from_numpy(X[r * b:(r + 1) * b]).cuda(),
                                   torch.from_numpy(Y[r * b:(r + 1) * b]).cuda())
-            out.append(gW[1].ravel())  # the 1024 x 1024 layer
+            out.append(gW[1].ravel())  # the second layer (2048 x 2048)
         return out
     finally:
         run.close()
@@ -48,18 +48,22 @@ def _exchange(w, grads, exchange):
 
 
 def test_sr16_unbiased_truncation_biased_on_real_gradients():
-    w = synth.with_batch(synth.C2, 256)
+    # 8192 rows per rank (the C3 bench's per-GPU batch at N = 4): every rank's gradient is a
+    # long sum with the same sign as the mean, the regime of P18 (with a few dozen rows per
+    # rank the ranks' signs disagree and the first stage's biases cancel in the mean)
+    w = synth.Workload("sig_2048", (2048, 2048, 2048), 4 * 8192, "MSE", 2.0 ** -2, "he")
     Ws, bs = synth.init_params(w)
     grads = _per_rank_grads(w, Ws, bs)
     ref = _exchange(w, grads, "FP32").astype(np.float64)
     sel = np.abs(ref) > 1e-3 * np.max(np.abs(ref))  # away from exact cancellation
     t16 = _exchange(w, grads, "TRUNC16").astype(np.float64)
     sr16 = _exchange(w, grads, "SR16").astype(np.float64)
-    bias_t = float(np.mean((t16[sel] - ref[sel]) / np.abs(ref[sel])))
-    bias_s = float(np.mean((sr16[sel] - ref[sel]) / np.abs(ref[sel])))
+    # signed relative error (g_hat - g) / g: < 0 when the magnitude shrinks, whatever the sign
+    bias_t = float(np.mean((t16[sel] - ref[sel]) / ref[sel]))
+    bias_s = float(np.mean((sr16[sel] - ref[sel]) / ref[sel]))
     print({"trunc16_mean_rel": bias_t, "sr16_mean_rel": bias_s, "elements": int(sel.sum())})
-    assert -8e-3 < bias_t < -2.5e-3, bias_t      # two truncations toward zero (P18)
-    assert abs(bias_s) < 1e-3, bias_s            # unbiased (reading A26)
+    assert -8e-3 < bias_t < -2e-3, bias_t                 # two truncations toward zero (P18)
+    assert abs(bias_s) < 0.1 * abs(bias_t), (bias_s, bias_t)  # unbiased (reading A26)
     # both within the two-stage bound, element by element: stage 1 moves each g_r by < 2^-7 |g_r|,
     # stage 2 the mean by < 2^-7 of itself: |g_hat - mean| < 2^-7 (A + |mean| + 2^-7 A),
     # A = sum_r |g_r| / N (SR16's draws move a value by less than one bf16 ulp as well)
