@@ -293,3 +293,30 @@ def test_sim_dead_peer_poisons_within_timeout(monkeypatch):
             assert st == D.DFLOW_SESSION_POISONED, D.STATUS.get(st)
     finally:
         run.close()
+
+
+def test_rejected_step_changes_nothing():
+    """A step rejected by its argument checks (here: the MSE target not fed) returns
+    DFLOW_INVALID_ARGUMENT on every rank before anything is enqueued and does not advance the
+    step counter that keys the flags and the SR16 draws: the next good step gives exactly the
+    bits of a world that never saw the bad call (SR16 over the fused channel, N = 4)."""
+    w = synth.with_batch(synth.C2, 256)
+    world = 4
+    b = w.batch // world
+    Ws, bs = synth.init_params(w)
+    Xs, Ys, _, _ = _rank_feeds(w, world)
+    res = []
+    for bad in (True, False):
+        run = SimRun(w.dims, "MSE", w.lr, rows=b, world=world, exchange="SR16", p2p=1, sr_seed=SEED)
+        try:
+            run.assign(Ws, bs)
+            if bad:
+                with pytest.raises(D.DflowError) as e:
+                    run.step(Xs, None)
+                assert e.value.status == D.DFLOW_INVALID_ARGUMENT
+            run.step(Xs, Ys)
+            run.step(Xs, Ys)
+            res.append(run.read(0))
+        finally:
+            run.close()
+    assert all(_bits_equal(a, c) for a, c in zip(res[0][0] + res[0][1], res[1][0] + res[1][1]))

@@ -346,3 +346,20 @@ def test_raster_group_leaves_results_bitwise(monkeypatch):
     assert l0 == l1
     for a, b in zip(W0 + b0, W1 + b1):
         assert np.array_equal(a, b)
+
+
+def test_loss_bitwise_reproducible_under_dynamic_scheduler():
+    """The cost is summed from one fp64 partial per (tile, CTA, epilogue warp) in a fixed
+    order, so repeated forwards give the same bits even though the dynamic tile scheduler
+    hands tiles to different CTAs each time (C3 width, B = 2048: CTA-pair loss epilogue)."""
+    w = with_batch(C3, 2048)
+    Ws, bs = init_params(w)
+    X, Y = batch(w)
+    run = Run(w.dims, w.loss, w.lr, rows=w.batch)
+    try:
+        run.assign(Ws, bs)
+        Xd, Yd = _dev(X), _dev(Y)
+        vals = {run.forward(Xd, Yd)[0].tobytes() for _ in range(8)}
+        assert len(vals) == 1
+    finally:
+        run.close()
