@@ -302,7 +302,7 @@ def run_gpu(args, w):
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            step(C.byref(step_loss))  # every step's loss is read back (inside the region)
+            step(C.byref(step_loss) if args.step_loss else None)  # the loss read back every step
         # defer_apply: the last step's pending updates belong to the region
         D.check(D.dflow_session_sync(s, sp))
         e1.record(stream)
@@ -439,6 +439,7 @@ def run_gpu(args, w):
                     "blocking_value": w.batch * e2e_steps / e2e_blocking_s,
                     "pipelined_value": w.batch * e2e_steps / e2e_pipelined_s},
             "gpu_launches": launches * args.steps,
+            "loss_read_every_step": bool(args.step_loss),
             "gather": ("nvlink_multicast" if st.multicast else "unicast") if world > 1 else None,
             "clocks": clk,
             "loss": {"first": first_loss.value, "last": last_loss.value},
@@ -542,6 +543,8 @@ def main():
                          "buffers), 0 = NCCL alltoall/allgather")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--step-loss", type=int, default=1,
+                    help="1: every timed step reads its loss back to the host (part of the region); 0: none")
     ap.add_argument("--c5-sub", type=int, default=1,
                     help="N = 1: also measure C5 (16 x 4096^2, 3xTF32, B = 65536) and report it as c5_3xtf32_n1")
     args = ap.parse_args()

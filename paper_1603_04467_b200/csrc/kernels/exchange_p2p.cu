@@ -56,13 +56,14 @@ __device__ __noinline__ bool wait_flags_bounded(const uint32_t* flags, int n, ui
 }
 
 // thread 0 of the block waits for flags[0..n) >= epoch; the block proceeds (true) or gives up
-// together (false)
+// together (false).  The verdict travels through the barrier's reduction, not shared memory:
+// these kernels must use NO shared memory, or they cannot sit on an SM beside a resident GEMM
+// CTA (227 KB dynamic + 1 KB static of the SM's 228 KB) and the exchange stops overlapping
+// the backward.
 __device__ __forceinline__ bool block_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint32_t* abort,
                                                  uint64_t timeout_ns) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) ok = wait_flags_bounded(flags, n, epoch, abort, timeout_ns) ? 1 : 0;
-  __syncthreads();
-  return ok != 0;
+  const bool ok = threadIdx.x != 0 || wait_flags_bounded(flags, n, epoch, abort, timeout_ns);
+  return __syncthreads_and(ok) != 0;
 }
 
 // The block's peer stores are ordered before thread 0 by the CTA barrier; thread 0's
