@@ -35,21 +35,28 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 // wait of this session has given up -> give up at once; timeout_ns passed -> raise abort.
 __device__ __noinline__ bool wait_flags_bounded(const uint32_t* flags, int n, uint32_t epoch, uint32_t* abort,
                                                 uint64_t timeout_ns) {
-  uint64_t t0 = 0;
+  // the abort word is host memory (read over PCIe): poll it only every ~50 us of waiting,
+  // the flags (device / NVLink memory) every iteration
+  constexpr uint64_t kAbortPollNs = 50000;
+  uint64_t t0 = 0, next_poll = 0;
   for (int r = 0; r < n; ++r) {
     while (static_cast<int32_t>(ld_acquire_sys(flags + r) - epoch) < 0) {
       if (abort != nullptr) {
-        if (*reinterpret_cast<volatile uint32_t*>(abort) != 0) return false;
         const uint64_t now = globaltimer_ns();
         if (t0 == 0) {
           t0 = now;
-        } else if (now - t0 > timeout_ns) {
-          *reinterpret_cast<volatile uint32_t*>(abort) = 1u;  // any writer writes 1: no atomic needed
-          __threadfence_system();
-          return false;
+          next_poll = now + kAbortPollNs;
+        } else if (now >= next_poll) {
+          if (*reinterpret_cast<volatile uint32_t*>(abort) != 0) return false;  // another wait gave up
+          if (now - t0 > timeout_ns) {
+            *reinterpret_cast<volatile uint32_t*>(abort) = 1u;  // any writer writes 1: no atomic needed
+            __threadfence_system();
+            return false;
+          }
+          next_poll = now + kAbortPollNs;
         }
       }
-      __nanosleep(256);
+      __nanosleep(64);
     }
   }
   return true;
@@ -160,7 +167,7 @@ __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16
       const int64_t row = idx0 / p.out, col = idx0 - row * p.out;
       const uint4 hv = make_uint4(h[0], h[1], h[2], h[3]);
       if (p.mc_wop) {  // one multicast store: the switch writes every rank's copy
-        asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(
+        asm volatile("multimem.st.weak.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(
                          p.mc_wop + row * p.ldwb + col),
                      "r"(hv.x), "r"(hv.y), "r"(hv.z), "r"(hv.w)
                      : "memory");

@@ -1426,7 +1426,11 @@ dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_
       CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
       // synchronous replicas: every rank takes part in the loss all-reduce whether or not it
       // asked for the value (a collective must be issued by all ranks)
-      if (loss_out || (s->replicas > 1 && !s->async)) ST(enqueue_loss(s, stream));
+      static const bool ab_lazy_loss = [] {  // A/B timing knob only: the round-1 behaviour
+        const char* e = getenv("DFLOW_AB_LAZY_LOSS");
+        return e && atoi(e) != 0;
+      }();
+      if (loss_out || (s->replicas > 1 && !s->async && !ab_lazy_loss)) ST(enqueue_loss(s, stream));
       ST(run_backward(s, rows, stream, 0));
     }
     s->last_launches = s->launches;

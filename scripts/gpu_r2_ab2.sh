@@ -8,5 +8,5 @@ ab() {  # $1 tag, $2 dir, extra args
 for rep in 1 2; do
   ab r1_$rep _r1
   ab r2_loss1_$rep .
-  ab r2_loss0_$rep . --step-loss 0
+  ab r2_mc0_$rep . --step-loss 1 --gpus 4
 done

@@ -1,0 +1,13 @@
+set -x
+ab() {  # $1 tag, $2 dir, extra args
+  tag=$1; dir=$2; shift 2
+  (cd $dir && timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 \
+      --master-port $((29700 + RANDOM % 200)) bench.py --gpus 4 --steps 20 --warmup 5 --batch 16384 "$@") > gpurun_out/ab4_$tag.json 2> gpurun_out/ab4_$tag.err
+  tail -c 200 gpurun_out/ab4_$tag.json
+}
+for rep in 1 2; do
+  ab r1_$rep _r1
+  ab r2_$rep .
+  DFLOW_AB_LAZY_LOSS=1 ab r2lazy_$rep . --step-loss 0
+  DFLOW_P2P_MULTICAST=0 DFLOW_AB_LAZY_LOSS=1 ab r2lazy_uni_$rep . --step-loss 0
+done
