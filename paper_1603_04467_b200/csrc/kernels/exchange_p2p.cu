@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "colsum.cuh"
 #include "exchange_p2p.h"
@@ -30,30 +31,26 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
-// One thread waits until flags[0..n) >= epoch.  The fast path is the flag load alone; only
-// while a flag is behind does it read the abort word (host memory) and the clock: another
-// wait of this session has given up -> give up at once; timeout_ns passed -> raise abort.
+// One thread waits until flags[0..n) >= epoch.  The loop is round 1's: the flag load and a
+// short sleep.  Only every 2^14 iterations (~2 ms of waiting) does it look at the clock and
+// the abort word (host memory, read over PCIe): another wait of this session has given up ->
+// give up at once; timeout_ns passed -> raise abort.  (Reading %globaltimer and the abort word
+// on every iteration slowed the 8-GPU proxy step by 3.5 %: profiles/r2/ab_r1_r2.)
 __device__ __noinline__ bool wait_flags_bounded(const uint32_t* flags, int n, uint32_t epoch, uint32_t* abort,
                                                 uint64_t timeout_ns) {
-  // the abort word is host memory (read over PCIe): poll it only every ~50 us of waiting,
-  // the flags (device / NVLink memory) every iteration
-  constexpr uint64_t kAbortPollNs = 50000;
-  uint64_t t0 = 0, next_poll = 0;
+  uint64_t t0 = 0;
+  uint32_t spins = 0;
   for (int r = 0; r < n; ++r) {
     while (static_cast<int32_t>(ld_acquire_sys(flags + r) - epoch) < 0) {
-      if (abort != nullptr) {
+      if (abort != nullptr && (++spins & 0x3FFFu) == 0) {
+        if (*reinterpret_cast<volatile uint32_t*>(abort) != 0) return false;  // another wait gave up
         const uint64_t now = globaltimer_ns();
         if (t0 == 0) {
           t0 = now;
-          next_poll = now + kAbortPollNs;
-        } else if (now >= next_poll) {
-          if (*reinterpret_cast<volatile uint32_t*>(abort) != 0) return false;  // another wait gave up
-          if (now - t0 > timeout_ns) {
-            *reinterpret_cast<volatile uint32_t*>(abort) = 1u;  // any writer writes 1: no atomic needed
-            __threadfence_system();
-            return false;
-          }
-          next_poll = now + kAbortPollNs;
+        } else if (now - t0 > timeout_ns) {
+          *reinterpret_cast<volatile uint32_t*>(abort) = 1u;  // any writer writes 1: no atomic needed
+          __threadfence_system();
+          return false;
         }
       }
       __nanosleep(64);
@@ -99,6 +96,37 @@ __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int
                     (threadIdx.x & 7);
   const float sum = colsum_warp(ws, chunks, cols, c);
   if ((threadIdx.x & 31) < 8 && c < cols) {
+    const int64_t idx = base_idx + c;
+    const int owner = static_cast<int>(idx / p.shard);
+    p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
+        static_cast<uint16_t>(round16(__float_as_uint(sum), idx, r16));
+  }
+  grid_signal(p, 0, epoch);
+}
+
+// A/B timing only (DFLOW_AB_OLD_COLSUM=1): round 1's db pass — one thread per column, 64-thread
+// blocks, a different summation order (db bits then differ from the fetched gradient's)
+__global__ void k_colsum_final_p2p_r1(const float* __restrict__ ws, int chunks, int64_t cols, int64_t base_idx,
+                                      const P2PLayer p, uint32_t epoch, Round16 r16) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (c < cols) {
+    float t[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t[g] = 0.f;
+    int k0 = 0;
+    for (; k0 + 8 <= chunks; k0 += 8) {
+      float a[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) a[g] = ws[static_cast<int64_t>(k0 + g) * cols + c];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) t[g] = __fadd_rn(t[g], a[g]);
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (k0 + g < chunks) t[g] = __fadd_rn(t[g], ws[static_cast<int64_t>(k0 + g) * cols + c]);
+    float sum = t[0];
+#pragma unroll
+    for (int g = 1; g < 8; ++g) sum = __fadd_rn(sum, t[g]);
     const int64_t idx = base_idx + c;
     const int owner = static_cast<int>(idx / p.shard);
     p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
@@ -215,6 +243,15 @@ __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint3
 
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
                                     uint32_t epoch, cudaStream_t s, Round16 r) {
+  static const bool ab_old = [] {
+    const char* e = getenv("DFLOW_AB_OLD_COLSUM");
+    return e && atoi(e) != 0;
+  }();
+  if (ab_old) {
+    k_colsum_final_p2p_r1<<<static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64)), 64, 0, s>>>(
+        ws, chunks, cols, base_idx, p, epoch, r);
+    return cudaGetLastError();
+  }
   // 8 warps x 8 columns per block: few blocks, so few system-scope fences in grid_signal
   const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64));
   k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);

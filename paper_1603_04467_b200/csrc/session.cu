@@ -473,6 +473,8 @@ dflow_status setup_p2p(dflow_session* s) {
     ly.p2p.rank = R;
     ly.p2p.world = N;
     ly.p2p.abort = s->abort_dev;
+    if (const char* e = getenv("DFLOW_AB_UNBOUNDED_WAIT"))  // A/B timing only: round 1's plain spin
+      if (atoi(e) != 0) ly.p2p.abort = nullptr;
     ly.p2p.timeout_ns = s->flag_timeout_ns;
   }
   if (s->tf32) return DFLOW_OK;
@@ -640,6 +642,11 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     f.max_ctas = max_ctas;
     f.group = raster_group("DFLOW_GEMM_GROUP_FWD", kGroupFwd);
     f.sched = s->sched_fd;  // this session's own counters (never another session's stream)
+    static const bool ab_shared_sched = [] {  // A/B timing only: round 1's per-device counters
+      const char* e = getenv("DFLOW_AB_SHARED_SCHED");
+      return e && atoi(e) != 0;
+    }();
+    if (ab_shared_sched) f.sched = nullptr;
     if (!last) {
       f.epilogue = EPI_BIAS_RELU;
       f.out = ly.A.hi; f.out2 = ly.A.lo; f.ldo = ly.ld_out;
@@ -681,7 +688,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
       d.group = raster_group("DFLOW_GEMM_GROUP_DGRAD", kGroupDgrad);
-      d.sched = s->sched_fd + 2;
+      d.sched = ab_shared_sched ? nullptr : s->sched_fd + 2;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
       if (s->mp && l == s->mp_lo) {  // f4: dA_{l-1} crosses back to rank-1 as channel codes (no mask here)
@@ -756,6 +763,10 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     if (ly.has_dgrad) dmax = std::max(dmax, ly.dgrad.grid);
   }
   s->bwd_side = s->replicas == 1 && !s->mp && s->L > 1 && wsum + dmax <= s->num_sms;
+  // A/B knob (DFLOW_BWD_SIDE = 0 / 1): force the side-stream dW schedule off / on (on large
+  // layers the persistent dW GEMM then only fills the SMs the dgrad's last wave leaves idle)
+  if (const char* e = getenv("DFLOW_BWD_SIDE"))
+    s->bwd_side = atoi(e) != 0 && s->replicas == 1 && !s->mp && s->L > 1;
   s->planned_rows = rows;
   return DFLOW_OK;
 }
