@@ -306,6 +306,13 @@ dflow_status dflow_gemm_3xtf32(int64_t M, int64_t N, int64_t K, const float* A_h
 /* The tf32 split itself (NK13, 3xTF32 path): hi = tf32_rna(src), lo = src - hi, n elements. */
 dflow_status dflow_split_tf32(const float* src, float* hi, float* lo, size_t n, void* stream);
 
+/* Die of every SM of `device` (0 / 1), measured once by L2 hit latencies: an SM reaches L2 lines
+ * homed on its own die faster than lines on the other die (B200: two dies, split L2).  The
+ * GEMM's tile scheduler uses it to keep each die on its own half of the output.  die_of_sm:
+ * [n] (SM id order); *agreement: the weakest SM's agreement with its die's near/far pattern.
+ * DFLOW_UNIMPLEMENTED when the measurement gives no clean two-die split.                  */
+dflow_status dflow_device_die_map(int32_t device, int32_t* die_of_sm, int32_t n, double* agreement);
+
 /* ------------------------------------------- simulated world (test harness)
  * The N-GPU replicated step (§7 :934-941; §5.5 :813-821 channel) run by N sessions
  * ("ranks") of one process on ONE GPU, so its kernels can be checked against the oracle on a

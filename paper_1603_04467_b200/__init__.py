@@ -108,6 +108,7 @@ _SIGS = {
                                _i64, _i32, _p]),
     "dflow_gemm_3xtf32": (_i32, [_i64, _i64, _i64, _p, _p, _i64, _i32, _p, _p, _i64, _i32, _p, _i64, _i32, _p]),
     "dflow_split_tf32": (_i32, [_p, _p, _p, _sz, _p]),
+    "dflow_device_die_map": (_i32, [_i32, C.POINTER(C.c_int32), _i32, C.POINTER(C.c_double)]),
     "dflow_sim_world_create": (_i32, [_i32, _i32, C.POINTER(_p)]),
     "dflow_sim_world_destroy": (None, [_p]),
     "dflow_sim_world_stream": (_i32, [_p, C.POINTER(_p)]),

@@ -16,6 +16,7 @@
 #include "graph.h"
 #include "kernels/elementwise.h"
 #include "kernels/gemm.h"
+#include "kernels/topology.h"
 #include "session.h"
 #include "sim.h"
 
@@ -457,6 +458,18 @@ dflow_status dflow_split_tf32(const float* src, float* hi, float* lo, size_t n, 
                                            static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return fail(DFLOW_CUDA, "split_tf32: %s", cudaGetErrorString(e));
   return DFLOW_OK;
+}
+
+dflow_status dflow_device_die_map(int32_t device, int32_t* die_of_sm, int32_t n, double* agreement) {
+  GUARD_BEGIN
+  std::vector<int> m;
+  double a = 0.0;
+  const bool ok = dflow::measure_die_map(device, &m, &a);
+  if (agreement) *agreement = a;
+  for (int i = 0; i < n && i < static_cast<int>(m.size()); ++i) if (die_of_sm) die_of_sm[i] = m[i];
+  if (m.empty()) return fail(DFLOW_CUDA, "die probe failed on device %d", device);
+  return ok ? DFLOW_OK : fail(DFLOW_UNIMPLEMENTED, "no clean two-die split (agreement %.3f)", a);
+  GUARD_END
 }
 
 // --------------------------------------------------------- simulated world (tests)

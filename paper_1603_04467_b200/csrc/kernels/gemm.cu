@@ -6,12 +6,15 @@
 #include <cstdio>
 #include <map>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
+#include <vector>
 
 #include "gemm.cuh"
 #include "gemm.h"
+#include "topology.h"
 
 namespace dflow {
 
@@ -111,7 +114,33 @@ static void* select_kernel(bool a_mn, bool b_mn, int epi, int* smem) {
   return nullptr;
 }
 
-// Tile-scheduler counters [counter, done] per (device, stream); zeroed once, and every GEMM
+// The measured SM -> die map of `dev` on the device (int per SM id), or NULL when the
+// measurement gave no clean two-die split; *n0 = SMs on die 0, *n = SMs.
+static const int* device_die_map(int dev, int* n0, int* n) {
+  static std::mutex mu;
+  static std::map<int, std::pair<int*, std::pair<int, int>>> maps;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = maps.find(dev);
+  if (it == maps.end()) {
+    std::vector<int> m;
+    int* d = nullptr;
+    int c0 = 0;
+    if (measure_die_map(dev, &m, nullptr) && cudaMalloc(&d, m.size() * sizeof(int)) == cudaSuccess) {
+      if (cudaMemcpy(d, m.data(), m.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        d = nullptr;
+      }
+      for (int x : m) c0 += x == 0;
+    }
+    cudaGetLastError();
+    it = maps.emplace(dev, std::make_pair(d, std::make_pair(c0, static_cast<int>(m.size())))).first;
+  }
+  *n0 = it->second.second.first;
+  *n = it->second.second.second;
+  return it->second.first;
+}
+
+// Tile-scheduler counters [die 0, die 1, done, pad] per (device, stream); zeroed once, and every GEMM
 // launch leaves them zero again, so launches serialised on one stream can share them (and
 // GEMMs on different streams never do).  Sessions pass their own counters in GemmDesc.sched.
 int* gemm_stream_sched(cudaStream_t stream) {
@@ -123,8 +152,8 @@ int* gemm_stream_sched(cudaStream_t stream) {
   int*& slot = ptrs[{dev, stream}];
   if (!slot) {
     void* p = nullptr;
-    if (cudaMalloc(&p, 2 * sizeof(int)) != cudaSuccess) return nullptr;
-    if (cudaMemset(p, 0, 2 * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMalloc(&p, 4 * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemset(p, 0, 4 * sizeof(int)) != cudaSuccess) return nullptr;
     slot = static_cast<int*>(p);
   }
   return slot;
@@ -294,6 +323,28 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   if (clusters > tiles) clusters = tiles;
   if (clusters < 1) clusters = 1;
   plan->grid = clusters * CG;
+  // die-aware schedule: split the raster in proportion to the dies' SMs (topology.cu);
+  // DFLOW_GEMM_DIE_SPLIT=0 turns it off (A/B)
+  a.die_map = nullptr;
+  a.die_split = tiles;
+  // experimental, off by default: +3 % sustained GEMM rate on one box, -6 % on another (the
+  // measured die map's quality varies per GPU) — DFLOW_GEMM_DIE_SPLIT=1 (two
+  // raster ranges) / 2 (N halves of every M-group)
+  static const int die_mode = [] {
+    const char* e = getenv("DFLOW_GEMM_DIE_SPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  int dev = 0;
+  if (die_mode && clusters == num_sms / CG && cudaGetDevice(&dev) == cudaSuccess) {
+    int n0 = 0, n = 0;
+    const int* dm = device_die_map(dev, &n0, &n);
+    if (dm && n == num_sms && (die_mode == 1 || plan->tiles_n >= 2)) {
+      a.die_map = dm;
+      a.die_mode = die_mode;
+      a.die_split = die_mode == 2 ? std::max(1, std::min(plan->tiles_n - 1, (plan->tiles_n * n0 + n / 2) / n))
+                                  : static_cast<int>((static_cast<int64_t>(tiles) * n0 + n / 2) / n);
+    }
+  }
   return cudaSuccess;
 }
 

@@ -455,7 +455,51 @@ __global__ void __launch_bounds__(256, 1)
     if (cta_rank == 0 && lane == 0) {
       int slot = 0;
       uint32_t ph = 0;
-      int t = cluster_id;
+      // Die-aware dynamic schedule (args.die_map; experimental, off by default): the raster's tiles are split
+      // at args.die_split into [0, split) for the clusters on die 0 and [split, num_tiles) for
+      // die 1 (in proportion to the dies' clusters), so the operand panels of a die's tiles are
+      // fetched across the die-to-die fabric once, not by both dies; a cluster draws from its
+      // own die's counter (sched[die]) and steals from the other's once its own is exhausted.
+      // Without a die map one range holds every tile.
+      int my_die = 0;
+      if (args.die_map) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        my_die = args.die_map[sm] & 1;
+      }
+      const int split = args.die_map ? args.die_split : num_tiles;
+      // die_mode 2: instead of two ranges of the raster, the two dies sweep the same M-groups
+      // side by side, die 0 over N-tiles [0, split), die 1 over [split, tiles_n): the A panels
+      // of a group are shared by both dies, every B panel is read by one die only
+      const bool nsplit = args.die_map && args.die_mode == 2;
+      const int tm_n = args.tiles_m, tn_n = args.tiles_n, grp = args.group_m;
+      auto nsplit_tile = [&](int d, int i) -> int {  // the i-th tile of die d -> raster id
+        const int n_lo = d ? split : 0, nd = d ? tn_n - split : split;
+        const int last_g = (tm_n - 1) / grp;
+        const int g = min(i / (grp * nd), last_g);
+        const int r = i - g * grp * nd;
+        const int gsize = min(tm_n - g * grp, grp);
+        const int m_off = r % gsize, n = n_lo + r / gsize;
+        return g * grp * tn_n + n * gsize + m_off;
+      };
+      auto draw = [&]() -> int {
+        for (int k = 0; k < 2; ++k) {
+          const int d = my_die ^ k;
+          int lo, hi;
+          if (nsplit) {
+            lo = 0;
+            hi = tm_n * (d ? tn_n - split : split);
+          } else {
+            lo = d ? split : 0;
+            hi = d ? num_tiles : split;
+          }
+          if (hi <= lo) continue;
+          const int i = atomicAdd(&args.sched[d], 1);
+          if (lo + i < hi) return nsplit ? nsplit_tile(d, i) : lo + i;
+        }
+        return num_tiles;
+      };
+      int t = args.sched ? draw() : cluster_id;
       for (;;) {
         ptx::mbar_wait(ptx::smem_u32(&sched_empty[slot]), ph ^ 1);
 #pragma unroll
@@ -468,7 +512,7 @@ __global__ void __launch_bounds__(256, 1)
           ptx::mbar_arrive_cluster(full_addr);
         }
         if (t >= num_tiles) break;
-        t = args.sched ? num_clusters + atomicAdd(&args.sched[0], 1) : t + num_clusters;
+        t = args.sched ? draw() : t + num_clusters;
         if (++slot == SD) {
           slot = 0;
           ph ^= 1;
@@ -477,9 +521,10 @@ __global__ void __launch_bounds__(256, 1)
       if (args.sched) {
         // the last cluster to finish resets the counters for the next launch on this stream
         __threadfence();
-        if (atomicAdd(&args.sched[1], 1) == num_clusters - 1) {
+        if (atomicAdd(&args.sched[2], 1) == num_clusters - 1) {
           atomicExch(&args.sched[0], 0);
           atomicExch(&args.sched[1], 0);
+          atomicExch(&args.sched[2], 0);
         }
       }
     }

@@ -57,7 +57,12 @@ struct GemmArgs {
   int debug;              // profiling only (DFLOW_GEMM_DEBUG): 1 no TMA loads, 2 no epilogue work,
                           // 4 hint-free barrier waits in the producer / MMA loop,
                           // 8 EPI_BIAS_RELU_LOSS targets not loaded (y = 0)
-  int* sched;             // [2] dynamic tile counter + done counter (zero at launch; the kernel resets them)
+  int* sched;             // [4]: tile counters of die 0 / die 1, done counter, pad (zero at launch; the
+                          // kernel resets them)
+  const int* die_map;     // [#SMs] die of each SM id (die-aware schedule), or NULL
+  int die_split;          // die_mode 1: raster tiles [0, die_split) to die 0, the rest to die 1;
+                          // die_mode 2: N-tiles [0, die_split) of every M-group to die 0
+  int die_mode;
   float seed_const;       // 1 / rows (SUM seed)
   float sgd_lr;           // EPI_SGD_APPLY learning rate
   double* loss_partials;  // [tiles * CG * 4] per-(tile, CTA, epilogue warp) partial sums
@@ -107,7 +112,7 @@ struct GemmDesc {
   int group;       // tile-raster group (M tiles); 0 = default
   int tile;        // 0 = auto, 1 = 128x128 (1 CTA), 2 = 256x256 (CTA pair)
   int max_ctas;    // 0 = all SMs; else cap (SM reservation for concurrent NCCL kernels)
-  int* sched;      // tile-scheduler counters [2] (zeroed); NULL = those of the device's legacy
+  int* sched;      // tile-scheduler counters [4] (zeroed); NULL = those of the device's legacy
                    // stream.  GEMMs that may run concurrently must not share counters
 };
 

@@ -405,7 +405,7 @@ dflow_status alloc_state(dflow_session* s) {
     const double ms = (e && atof(e) > 0) ? atof(e) : 60000.0;
     s->flag_timeout_ns = static_cast<uint64_t>(ms * 1e6);
   }
-  ST(dmalloc(s, &s->sched_fd, 4));  // zeroed: forward and dgrad plans of this session
+  ST(dmalloc(s, &s->sched_fd, 8));  // zeroed: forward [0, 4) and dgrad [4, 8) plans of this session
   s->ev_grad.resize(s->L);
   s->ev_apply.resize(s->L);
   for (int l = 0; l < s->L; ++l) {
@@ -430,7 +430,7 @@ dflow_status alloc_state(dflow_session* s) {
       return fail(DFLOW_CUDA, "stream creation failed");
     cudaEventCreateWithFlags(&s->ev_side_join[i], cudaEventDisableTiming);
   }
-  ST(dmalloc(s, &s->sched_w, 4));  // zeroed
+  ST(dmalloc(s, &s->sched_w, 8));  // zeroed: [4] per side stream
   return DFLOW_OK;
 }
 
@@ -688,7 +688,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
       d.group = raster_group("DFLOW_GEMM_GROUP_DGRAD", kGroupDgrad);
-      d.sched = ab_shared_sched ? nullptr : s->sched_fd + 2;
+      d.sched = ab_shared_sched ? nullptr : s->sched_fd + 4;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
       if (s->mp && l == s->mp_lo) {  // f4: dA_{l-1} crosses back to rank-1 as channel codes (no mask here)
@@ -708,7 +708,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     w.out_f32 = ly.g32; w.ldo32 = ly.out;
     w.max_ctas = max_ctas;
     w.group = raster_group("DFLOW_GEMM_GROUP_WGRAD", kGroupWgrad);
-    w.sched = s->sched_w + 2 * (l % 2);  // (bwd_side: dW_l runs on side[l % 2])
+    w.sched = s->sched_w + 4 * (l % 2);  // (bwd_side: dW_l runs on side[l % 2])
     ST(gemm_plan(s, w, &ly.wgrad32));
     if (s->replicas == 1 && s->trainable) {
       // no channel (reading A6): ApplyGradientDescent fused into the dW epilogue
@@ -1658,7 +1658,7 @@ dflow_status session_fetch_gradients(dflow_session* s, int n_feeds, const dflow_
         d.B = ly.Wop.hi; d.B2 = ly.Wop.lo; d.ldb = ly.ld_wb; d.b_mn = false;
         d.epilogue = EPI_F32;
         d.out_f32 = static_cast<float*>(out[i]); d.ldo32 = ly.in;
-        d.sched = s->sched_fd + 2;
+        d.sched = s->sched_fd + 4;
         GemmPlan p;
         ST(gemm_plan(s, d, &p));
         ST(launch_gemm(s, p, st));

@@ -104,7 +104,7 @@ struct dflow_session {
   // on side[l % 2], concurrently with the next dgrad and with dW_{l-1} (no shared buffers)
   cudaStream_t side[2] = {nullptr, nullptr};
   cudaEvent_t ev_side_join[2] = {nullptr, nullptr};
-  int* sched_w = nullptr;  // [2][2] tile-scheduler counters of the dW GEMMs, per side stream
+  int* sched_w = nullptr;  // [2][4] tile-scheduler counters of the dW GEMMs, per side stream
   bool bwd_side = false;
   cudaEvent_t ev_loss = nullptr;
   // loss value landed in loss_host[slot] (after the forward); two slots so a pipelined
@@ -147,7 +147,7 @@ struct dflow_session {
   uint32_t* abort_host = nullptr;
   uint32_t* abort_dev = nullptr;
   uint64_t flag_timeout_ns = 0;
-  int* sched_fd = nullptr;  // [2][2] tile-scheduler counters of this session's forward / dgrad GEMMs
+  int* sched_fd = nullptr;  // [2][4] tile-scheduler counters of this session's forward / dgrad GEMMs
   // f1 multicast (bf16 owner-apply over NCCL): every layer's bf16 W copy lives in one symmetric
   // NCCL window whose multicast address the owner fold stores through (comm.h)
   dflow::SymRegion* wsym = nullptr;
