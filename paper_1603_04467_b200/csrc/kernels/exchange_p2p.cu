@@ -104,37 +104,6 @@ __global__ void k_colsum_final_p2p(const float* __restrict__ ws, int chunks, int
   grid_signal(p, 0, epoch);
 }
 
-// A/B timing only (DFLOW_AB_OLD_COLSUM=1): round 1's db pass — one thread per column, 64-thread
-// blocks, a different summation order (db bits then differ from the fetched gradient's)
-__global__ void k_colsum_final_p2p_r1(const float* __restrict__ ws, int chunks, int64_t cols, int64_t base_idx,
-                                      const P2PLayer p, uint32_t epoch, Round16 r16) {
-  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (c < cols) {
-    float t[8];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) t[g] = 0.f;
-    int k0 = 0;
-    for (; k0 + 8 <= chunks; k0 += 8) {
-      float a[8];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) a[g] = ws[static_cast<int64_t>(k0 + g) * cols + c];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) t[g] = __fadd_rn(t[g], a[g]);
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-      if (k0 + g < chunks) t[g] = __fadd_rn(t[g], ws[static_cast<int64_t>(k0 + g) * cols + c]);
-    float sum = t[0];
-#pragma unroll
-    for (int g = 1; g < 8; ++g) sum = __fadd_rn(sum, t[g]);
-    const int64_t idx = base_idx + c;
-    const int owner = static_cast<int>(idx / p.shard);
-    p.recv[owner][static_cast<int64_t>(p.rank) * p.shard + (idx - static_cast<int64_t>(owner) * p.shard)] =
-        static_cast<uint16_t>(round16(__float_as_uint(sum), idx, r16));
-  }
-  grid_signal(p, 0, epoch);
-}
-
 __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16) {
   // every rank's contribution has landed (or the wait timed out: no fold, no signal)
   if (!block_wait_flags(p.flags[p.rank], p.world, epoch, p.abort, p.timeout_ns)) return;
@@ -243,15 +212,6 @@ __global__ void k_wait_flags(const uint32_t* flags, int n, uint32_t epoch, uint3
 
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,
                                     uint32_t epoch, cudaStream_t s, Round16 r) {
-  static const bool ab_old = [] {
-    const char* e = getenv("DFLOW_AB_OLD_COLSUM");
-    return e && atoi(e) != 0;
-  }();
-  if (ab_old) {
-    k_colsum_final_p2p_r1<<<static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64)), 64, 0, s>>>(
-        ws, chunks, cols, base_idx, p, epoch, r);
-    return cudaGetLastError();
-  }
   // 8 warps x 8 columns per block: few blocks, so few system-scope fences in grid_signal
   const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, (cols + 63) / 64));
   k_colsum_final_p2p<<<blocks, 256, 0, s>>>(ws, chunks, cols, base_idx, p, epoch, r);

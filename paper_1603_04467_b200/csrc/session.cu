@@ -473,8 +473,6 @@ dflow_status setup_p2p(dflow_session* s) {
     ly.p2p.rank = R;
     ly.p2p.world = N;
     ly.p2p.abort = s->abort_dev;
-    if (const char* e = getenv("DFLOW_AB_UNBOUNDED_WAIT"))  // A/B timing only: round 1's plain spin
-      if (atoi(e) != 0) ly.p2p.abort = nullptr;
     ly.p2p.timeout_ns = s->flag_timeout_ns;
   }
   if (s->tf32) return DFLOW_OK;
@@ -642,11 +640,6 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
     f.max_ctas = max_ctas;
     f.group = raster_group("DFLOW_GEMM_GROUP_FWD", kGroupFwd);
     f.sched = s->sched_fd;  // this session's own counters (never another session's stream)
-    static const bool ab_shared_sched = [] {  // A/B timing only: round 1's per-device counters
-      const char* e = getenv("DFLOW_AB_SHARED_SCHED");
-      return e && atoi(e) != 0;
-    }();
-    if (ab_shared_sched) f.sched = nullptr;
     if (!last) {
       f.epilogue = EPI_BIAS_RELU;
       f.out = ly.A.hi; f.out2 = ly.A.lo; f.ldo = ly.ld_out;
@@ -688,7 +681,7 @@ dflow_status plan_rows(dflow_session* s, int64_t rows) {
       d.colsum_ws = lp.colsum_ws;  // db_{l-1} partials fused (a5)
       d.max_ctas = max_ctas;
       d.group = raster_group("DFLOW_GEMM_GROUP_DGRAD", kGroupDgrad);
-      d.sched = ab_shared_sched ? nullptr : s->sched_fd + 4;
+      d.sched = s->sched_fd + 4;
       ST(gemm_plan(s, d, &ly.dgrad));
       ly.has_dgrad = true;
       if (s->mp && l == s->mp_lo) {  // f4: dA_{l-1} crosses back to rank-1 as channel codes (no mask here)
@@ -1437,11 +1430,7 @@ dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_
       CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
       // synchronous replicas: every rank takes part in the loss all-reduce whether or not it
       // asked for the value (a collective must be issued by all ranks)
-      static const bool ab_lazy_loss = [] {  // A/B timing knob only: the round-1 behaviour
-        const char* e = getenv("DFLOW_AB_LAZY_LOSS");
-        return e && atoi(e) != 0;
-      }();
-      if (loss_out || (s->replicas > 1 && !s->async && !ab_lazy_loss)) ST(enqueue_loss(s, stream));
+      if (loss_out || (s->replicas > 1 && !s->async)) ST(enqueue_loss(s, stream));
       ST(run_backward(s, rows, stream, 0));
     }
     s->last_launches = s->launches;
