@@ -195,6 +195,25 @@ __global__ void k_owner_reduce_p2p(const P2PLayer p, uint32_t epoch, Round16 r16
   grid_signal(p, 1, epoch);
 }
 
+__global__ void k_loss_push(const float* __restrict__ loss, const LossPeers p, int rank, int world, uint32_t epoch) {
+  if (threadIdx.x != 0) return;
+  const float v = loss[0];
+  const int par = static_cast<int>(epoch & 1u);  // two slots: a fast rank's next push never meets an unread value
+  for (int j = 0; j < world; ++j) p.slots[j][par * kMaxRanks + rank] = v;
+  __threadfence_system();
+  for (int j = 0; j < world; ++j) st_release_sys(p.flags[j] + rank, epoch);
+}
+
+__global__ void k_loss_gather(const float* slots, const uint32_t* flags, int world, uint32_t epoch,
+                              float* __restrict__ out, uint32_t* abort, uint64_t timeout_ns) {
+  if (threadIdx.x != 0) return;
+  if (!wait_flags_bounded(flags, world, epoch, abort, timeout_ns)) return;
+  const volatile float* sl = slots + static_cast<int>(epoch & 1u) * kMaxRanks;
+  float sum = sl[0];
+  for (int r = 1; r < world; ++r) sum = __fadd_rn(sum, sl[r]);
+  out[0] = sum;
+}
+
 __global__ void k_gather_w32(const P2PLayer p) {
   const int64_t nw = p.in * p.out;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -222,6 +241,18 @@ cudaError_t launch_owner_reduce_p2p(const P2PLayer& p, uint32_t epoch, cudaStrea
   const int64_t nv = p.shard / 8;
   const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((nv + 255) / 256, 148 * 2)));
   k_owner_reduce_p2p<<<blocks, 256, 0, s>>>(p, epoch, r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_push(const float* loss, const LossPeers& p, int rank, int world, uint32_t epoch,
+                             cudaStream_t s) {
+  k_loss_push<<<1, 32, 0, s>>>(loss, p, rank, world, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_gather(const float* slots, const uint32_t* flags, int world, uint32_t epoch, float* out,
+                               uint32_t* abort, uint64_t timeout_ns, cudaStream_t s) {
+  k_loss_gather<<<1, 32, 0, s>>>(slots, flags, world, epoch, out, abort, timeout_ns);
   return cudaGetLastError();
 }
 

@@ -46,6 +46,19 @@ struct P2PLayer {
   uint64_t timeout_ns;
 };
 
+// The cost C = mean_r C_r of a synchronous step over the same peer memory (no NCCL call in the
+// step): every rank pushes its C_r into slot [epoch & 1][rank] of every rank and raises its
+// flag; a rank that wants the value sums the N slots in rank order once all flags reach epoch.
+struct LossPeers {
+  float* slots[kMaxRanks];     // rank j's [2][kMaxRanks] loss slots
+  uint32_t* flags[kMaxRanks];  // rank j's [kMaxRanks] loss flags
+};
+cudaError_t launch_loss_push(const float* loss, const LossPeers& p, int rank, int world, uint32_t epoch,
+                             cudaStream_t s);
+// out[0] = slots[par][0] + ... + slots[par][world-1] (fp32, rank order) once flags >= epoch
+cudaError_t launch_loss_gather(const float* slots, const uint32_t* flags, int world, uint32_t epoch, float* out,
+                               uint32_t* abort, uint64_t timeout_ns, cudaStream_t s);
+
 // db_l (sum of the per-32-row partials), coded (truncate / SR16) and stored at bucket index
 // base_idx + c in its owner's receive slot; then phase-0 flags.
 cudaError_t launch_colsum_final_p2p(const float* ws, int chunks, int64_t cols, int64_t base_idx, const P2PLayer& p,

@@ -453,13 +453,21 @@ dflow_status setup_p2p(dflow_session* s) {
     off_gath[l] = take(s->layers[l].Ppad * 2);
     off_flags[l] = take(2 * kMaxRanks * sizeof(uint32_t));
   }
+  const size_t off_loss = take((2 * kMaxRanks) * sizeof(float) + kMaxRanks * sizeof(uint32_t));
   CU(cudaMalloc(&s->sym, total));
   CU(cudaMemset(s->sym, 0, total));
   CU(cudaMalloc(&s->p2p_done, 2 * s->L * sizeof(int)));
   CU(cudaMemset(s->p2p_done, 0, 2 * s->L * sizeof(int)));
   std::vector<void*> all;
   ST(comm_share_ptrs(s, &s->sym, 1, &all, &s->ipc_opened));
-  for (int j = 0; j < N; ++j) s->peer_sym[j] = all[j];
+  for (int j = 0; j < N; ++j) {
+    s->peer_sym[j] = all[j];
+    float* ls = reinterpret_cast<float*>(static_cast<char*>(all[j]) + off_loss);
+    s->loss_peers.slots[j] = ls;
+    s->loss_peers.flags[j] = reinterpret_cast<uint32_t*>(ls + 2 * kMaxRanks);
+  }
+  if (cudaStreamCreateWithFlags(&s->loss_stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(DFLOW_CUDA, "stream creation failed");
   for (int l = 0; l < s->L; ++l) {
     Layer& ly = s->layers[l];
     for (int j = 0; j < N; ++j) {
@@ -1219,7 +1227,7 @@ cudaError_t record_event(dflow_session* s, cudaEvent_t e, cudaStream_t st) {
   return s->capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
 }
 
-dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
+dflow_status enqueue_loss(dflow_session* s, cudaStream_t st, bool want) {
   if (s->mp) {  // f4: the last rank computed C; every rank reports it
     ST(comm_broadcast_f32(s, s->loss_dev, 1, s->opt.world - 1, st));
     CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, st));
@@ -1227,7 +1235,23 @@ dflow_status enqueue_loss(dflow_session* s, cudaStream_t st) {
     s->loss_pending[s->loss_slot] = true;
     return DFLOW_OK;
   }
-  if (s->replicas > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
+  if (s->replicas > 1 && !s->async && s->p2p) {
+    // fused channel: push C_r to every rank (always: a rank's peers may want the mean), gather
+    // the N values only when this caller wants C — no collective, so ranks may differ
+    ST(check_launch(s, launch_loss_push(s->loss_dev, s->loss_peers, s->opt.rank, s->opt.world, s->epoch, st), 1,
+                    "loss push"));
+    if (!want) return DFLOW_OK;
+    CU(cudaEventRecord(s->ev_loss, st));
+    CU(cudaStreamWaitEvent(s->loss_stream, s->ev_loss, 0));
+    ST(comm_rendezvous(s));  // (simulated world: every rank's push is enqueued first)
+    ST(check_launch(s, launch_loss_gather(s->loss_peers.slots[s->opt.rank], s->loss_peers.flags[s->opt.rank],
+                                          s->opt.world, s->epoch, s->loss_dev + 1, s->abort_dev,
+                                          s->flag_timeout_ns, s->loss_stream),
+                    1, "loss gather"));
+    CU(cudaMemcpyAsync(s->loss_host + s->loss_slot, s->loss_dev + 1, sizeof(float), cudaMemcpyDeviceToHost,
+                       s->loss_stream));
+    CU(cudaEventRecord(s->ev_loss_ready[s->loss_slot], s->loss_stream));
+  } else if (s->replicas > 1 && !s->async) {  // (asynchronous replicas report their own C_r)
     CU(cudaEventRecord(s->ev_loss, st));
     CU(cudaStreamWaitEvent(s->comm, s->ev_loss, 0));
     ST(comm_allreduce_f32(s, s->loss_dev, s->loss_dev + 1, 1, s->comm));
@@ -1390,6 +1414,7 @@ void session_destroy(dflow_session* s) {
     if (s->ev_side_join[i]) cudaEventDestroy(s->ev_side_join[i]);
   }
   if (s->comm && s->comm_owned) cudaStreamDestroy(s->comm);
+  if (s->loss_stream) cudaStreamDestroy(s->loss_stream);
   cudaGetLastError();
   delete s;
 }
@@ -1423,14 +1448,15 @@ dflow_status session_train_step_impl(dflow_session* s, int n_feeds, const dflow_
       ST(run_forward_mp(s, f, rows, stream));
       CU(record_event(s, s->ev_x_free, stream));
       CU(record_event(s, s->ev_feeds_free, stream));
-      ST(enqueue_loss(s, stream));  // every rank takes part in the loss broadcast
+      ST(enqueue_loss(s, stream, true));  // every rank takes part in the loss broadcast
       ST(run_backward_mp(s, rows, stream));
     } else {
       ST(run_forward(s, f, rows, stream, FWD_TRAIN));
       CU(record_event(s, s->ev_feeds_free, stream));  // x and y are not read after the forward
-      // synchronous replicas: every rank takes part in the loss all-reduce whether or not it
-      // asked for the value (a collective must be issued by all ranks)
-      if (loss_out || (s->replicas > 1 && !s->async)) ST(enqueue_loss(s, stream));
+      // synchronous replicas: every rank takes part in the loss exchange whether or not it
+      // asked for the value (the NCCL schedule's all-reduce is a collective; the fused
+      // channel's push is one-sided and only a caller that wants C gathers)
+      if (loss_out || (s->replicas > 1 && !s->async)) ST(enqueue_loss(s, stream, loss_out != nullptr));
       ST(run_backward(s, rows, stream, 0));
     }
     s->last_launches = s->launches;

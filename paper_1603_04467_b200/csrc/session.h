@@ -152,6 +152,10 @@ struct dflow_session {
   // NCCL window whose multicast address the owner fold stores through (comm.h)
   dflow::SymRegion* wsym = nullptr;
   bool multicast = false;
+  // the cost's cross-replica mean over peer memory (fused channel, no NCCL call in the step):
+  // every rank's loss slots / flags in its symmetric allocation; the gather runs on loss_stream
+  dflow::LossPeers loss_peers{};
+  cudaStream_t loss_stream = nullptr;
   // fused NVLink exchange (opt.p2p): one symmetric allocation per rank, peers via CUDA IPC
   bool p2p = false;
   bool async = false;  // opt.async_dp (f3): sym holds this rank's parameter shards
