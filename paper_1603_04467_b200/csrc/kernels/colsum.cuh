@@ -52,4 +52,33 @@ __device__ __forceinline__ float colsum_warp(const float* __restrict__ ws, int c
   return s;
 }
 
+// The same t_g with more threads per column, for the kernels that may use shared memory:
+// lane (co, q) of warp-set s accumulates the groups g = q + 4 j for j in {2 s, 2 s + 1}; the
+// caller gathers t_0 .. t_31 and folds them in g order (identical arithmetic to colsum_warp).
+__device__ __forceinline__ void colsum_groups2(const float* __restrict__ ws, int chunks, int64_t cols, int64_t c,
+                                               int s, float (&t)[2]) {
+  const int q = (threadIdx.x & 31) >> 3;
+  t[0] = t[1] = 0.f;
+  if (c >= cols) return;
+  const int g0 = q + 8 * s, g1 = g0 + 4;  // j = 2s, 2s+1
+  int kb = 0;
+  for (; kb + 128 <= chunks; kb += 128) {  // four rounds of 32 chunks, 8 loads in flight
+    float a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = ws[static_cast<int64_t>(kb + 32 * u + g0) * cols + c];
+      b[u] = ws[static_cast<int64_t>(kb + 32 * u + g1) * cols + c];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      t[0] = __fadd_rn(t[0], a[u]);
+      t[1] = __fadd_rn(t[1], b[u]);
+    }
+  }
+  for (; kb < chunks; kb += 32) {
+    if (kb + g0 < chunks) t[0] = __fadd_rn(t[0], ws[static_cast<int64_t>(kb + g0) * cols + c]);
+    if (kb + g1 < chunks) t[1] = __fadd_rn(t[1], ws[static_cast<int64_t>(kb + g1) * cols + c]);
+  }
+}
+
 }  // namespace dflow

@@ -183,21 +183,21 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// One block of 256 threads: thread t sums partials t, t+256, ... in order, then the 8 warps'
-// shuffle trees and the 8 warp sums in warp order — a fixed summation order for a fixed n
+// One block of 1024 threads: thread t sums partials t, t+1024, ... in order, then the 32 warps'
+// shuffle trees and the 32 warp sums in warp order — a fixed summation order for a fixed n
 // (the GEMM epilogue stores one partial per (tile, CTA, warp), so n and every slot are fixed).
-__global__ void k_loss_final(int kind, const double* __restrict__ partials, int n, int64_t rows, int64_t cols,
-                             float* __restrict__ loss) {
-  __shared__ double ws[8];
+__global__ void __launch_bounds__(1024) k_loss_final(int kind, const double* __restrict__ partials, int n,
+                                                     int64_t rows, int64_t cols, float* __restrict__ loss) {
+  __shared__ double ws[32];
   double v = 0.0;
-  for (int i = threadIdx.x; i < n; i += 256) v += partials[i];
+  for (int i = threadIdx.x; i < n; i += 1024) v += partials[i];
   v = warp_sum_d(v);
   if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
   __syncthreads();
   if (threadIdx.x == 0) {
     v = ws[0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) v += ws[w];
+    for (int w = 1; w < 32; ++w) v += ws[w];
     const double c = (kind == 0) ? v / (2.0 * static_cast<double>(rows) * static_cast<double>(cols))
                                  : v / static_cast<double>(rows);
     *loss = static_cast<float>(c);
@@ -208,17 +208,29 @@ __global__ void k_loss_final(int kind, const double* __restrict__ partials, int 
 __device__ __forceinline__ float sgd(float w, float lr, float g) { return __fsub_rn(w, __fmul_rn(lr, g)); }
 
 // ------------------------------------------------------------------ colsum (final pass)
-// The fixed summation order of colsum.cuh; a block of 256 threads covers 64 columns.
-__global__ void k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols, float* __restrict__ out32,
-                               uint16_t* __restrict__ out16, Round16 r16, int64_t idx_base,
-                               float* __restrict__ bias, float lr) {
-  const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) / 32 * kColsumColsPerWarp +
-                    (threadIdx.x & 7);
-  const float s = colsum_warp(ws, chunks, cols, c);
-  if ((threadIdx.x & 31) < 8 && c < cols) {
-    if (out32) out32[c] = s;
-    if (out16) out16[c] = static_cast<uint16_t>(round16(__float_as_uint(s), idx_base + c, r16));
-    if (bias) bias[c] = sgd(bias[c], lr, s);  // N = 1: ApplyGradientDescent on b_l (a9), fused
+// The fixed summation order of colsum.cuh with 16 threads per column: a block of 1024 threads
+// covers 64 columns; warp w handles columns 8 (w % 8) .. +7 and the groups of warp-set w / 8;
+// the 32 group sums meet in shared memory and lanes of warp-set 0 fold them in g order.
+__global__ void __launch_bounds__(1024) k_colsum_final(const float* __restrict__ ws, int chunks, int64_t cols,
+                                                       float* __restrict__ out32, uint16_t* __restrict__ out16,
+                                                       Round16 r16, int64_t idx_base, float* __restrict__ bias,
+                                                       float lr) {
+  __shared__ float tg[8][32][9];  // [column group][g][column] (+1 pad)
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cw = w & 7, s = w >> 3, co = lane & 7, q = lane >> 3;
+  const int64_t c = blockIdx.x * 64LL + cw * 8 + co;
+  float t[2];
+  colsum_groups2(ws, chunks, cols, c, s, t);
+  tg[cw][q + 8 * s][co] = t[0];
+  tg[cw][q + 8 * s + 4][co] = t[1];
+  __syncthreads();
+  if (s == 0 && q == 0 && c < cols) {
+    float sum = tg[cw][0][co];
+#pragma unroll
+    for (int g = 1; g < 32; ++g) sum = __fadd_rn(sum, tg[cw][g][co]);
+    if (out32) out32[c] = sum;
+    if (out16) out16[c] = static_cast<uint16_t>(round16(__float_as_uint(sum), idx_base + c, r16));
+    if (bias) bias[c] = sgd(bias[c], lr, sum);  // N = 1: ApplyGradientDescent on b_l (a9), fused
   }
 }
 
@@ -454,15 +466,15 @@ cudaError_t launch_copy_bf16(const __nv_bfloat16* src, int64_t lds, __nv_bfloat1
 
 cudaError_t launch_loss_final(int kind, const double* partials, int n, int64_t rows, int64_t cols, float* loss,
                               cudaStream_t s) {
-  k_loss_final<<<1, 256, 0, s>>>(kind, partials, n, rows, cols, loss);
+  k_loss_final<<<1, 1024, 0, s>>>(kind, partials, n, rows, cols, loss);
   return cudaGetLastError();
 }
 
 cudaError_t launch_colsum_final(const float* ws, int chunks, int64_t cols, float* out_f32, uint16_t* out_u16,
                                 cudaStream_t s, Round16 r, int64_t idx_base, float* bias, float lr) {
   if (cols == 0) return cudaSuccess;
-  k_colsum_final<<<static_cast<unsigned>((cols + 63) / 64), 256, 0, s>>>(ws, chunks, cols, out_f32, out_u16, r,
-                                                                          idx_base, bias, lr);
+  k_colsum_final<<<static_cast<unsigned>((cols + 63) / 64), 1024, 0, s>>>(ws, chunks, cols, out_f32, out_u16, r,
+                                                                           idx_base, bias, lr);
   return cudaGetLastError();
 }
 
