@@ -47,10 +47,23 @@ def main():
                                       mask.stride(0) if mask is not None else 0, 0, sp))
         return f
 
+    def split_wgrad(P):
+        kc = b // P
+        fns = [ours(w, w, kc, A[p * kc:], 1, dZ[p * kc:], 1, D.EPI_F32, o32=out32) for p in range(P)]
+
+        def f():
+            for fn in fns:
+                fn()
+        return f
+
     table = {
         "fwd": lambda: ours(b, w, w, A, 0, W, 1, D.EPI_BIAS_RELU, out=out_bf, bias_=bias),
         "dgrad": lambda: ours(b, w, w, dZ, 0, W, 0, D.EPI_RELUGRAD, out=out_bf, mask=A),
         "wgrad": lambda: ours(w, w, b, A, 1, dZ, 1, D.EPI_F32, o32=out32),
+        # the wgrad as P passes over K / P rows each (fp32 out rewritten per pass): does an
+        # L2-sized K chunk cut DRAM traffic enough to pay for the extra passes?
+        "wgrad_split4": lambda: split_wgrad(4),
+        "wgrad_split2": lambda: split_wgrad(2),
         "fwd_cublas": lambda: (lambda: torch.matmul(A, W, out=out_bf)),
         "dgrad_cublas": lambda: (lambda: torch.matmul(dZ, W.t(), out=out_bf)),
         "wgrad_cublas": lambda: (lambda: torch.matmul(A.t(), dZ, out=out_w16)),
