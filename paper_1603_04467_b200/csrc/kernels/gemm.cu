@@ -91,6 +91,24 @@ static void* kernel_ptr(int* smem) {
   return reinterpret_cast<void*>(k);
 }
 
+// The wide pair tile (BN = 512, bf16): the forward, dgrad and wgrad epilogues of the N = 1
+// step and the NCCL-schedule exchange (not the fused-channel or asynchronous epilogues).
+static void* select_kernel_512(bool a_mn, bool b_mn, int epi, int* smem) {
+  if (!a_mn && b_mn) {
+    if (epi == EPI_BIAS_RELU) return kernel_ptr<512, 2, false, false, true, EPI_BIAS_RELU>(smem);
+    if (epi == EPI_BIAS_RELU_LOSS) return kernel_ptr<512, 2, false, false, true, EPI_BIAS_RELU_LOSS>(smem);
+    if (epi == EPI_F32) return kernel_ptr<512, 2, false, false, true, EPI_F32>(smem);
+  } else if (!a_mn && !b_mn) {
+    if (epi == EPI_RELUGRAD) return kernel_ptr<512, 2, false, false, false, EPI_RELUGRAD>(smem);
+    if (epi == EPI_F32) return kernel_ptr<512, 2, false, false, false, EPI_F32>(smem);
+  } else if (a_mn && b_mn) {
+    if (epi == EPI_F32) return kernel_ptr<512, 2, false, true, true, EPI_F32>(smem);
+    if (epi == EPI_TRUNC16) return kernel_ptr<512, 2, false, true, true, EPI_TRUNC16>(smem);
+    if (epi == EPI_SGD_APPLY) return kernel_ptr<512, 2, false, true, true, EPI_SGD_APPLY>(smem);
+  }
+  return nullptr;
+}
+
 // The (operand majors, epilogue) combinations the MLP step uses, per tile config.
 template <int BN, int CG, bool TF32>
 static void* select_kernel(bool a_mn, bool b_mn, int epi, int* smem) {
@@ -185,11 +203,30 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   if (tile == 0) {
     const int64_t pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
     tile = (pair_tiles >= num_sms / 2) ? 2 : 1;
+    // the wide pair tile, 256 x 512 per CTA pair, where it fills the machine and the epilogue
+    // has a 512-wide variant.  DFLOW_GEMM_TILE512 (A/B knob): 0 off (default), 1 every GEMM
+    // kind, 2 the weight gradient only.  It reads 25 % fewer operand bytes per FLOP and runs
+    // at a higher power-capped clock, but its single TMEM accumulator exposes the epilogue
+    // drain at every tile boundary: the N = 1 step is 5 % slower with it everywhere and
+    // unchanged with it on the weight gradient only
+    static const int wide = [] {
+      const char* e = getenv("DFLOW_GEMM_TILE512");
+      return e ? atoi(e) : 0;
+    }();
+    int dummy = 0;
+    const bool wgrad_kind = d.a_mn && d.b_mn;
+    if ((wide == 1 || (wide == 2 && wgrad_kind)) && tile == 2 && !d.tf32 &&
+        ((d.M + 255) / 256) * ((d.N + 511) / 512) >= num_sms / 2 && select_kernel_512(d.a_mn, d.b_mn, d.epilogue, &dummy))
+      tile = 3;
   }
   const bool tf = d.tf32;
+  if (tile == 3 && tf) {
+    snprintf(g_err, sizeof g_err, "the 512-wide tile is bf16 only");
+    return cudaErrorInvalidValue;
+  }
   // 3xTF32 pairs use N = 128 so the epilogue can hold a row's fp32 K-chunk sums in registers
-  const int BN = (tile == 2 && !tf) ? 256 : 128;
-  const int CG = (tile == 2) ? 2 : 1;
+  const int BN = tile == 3 ? 512 : (tile == 2 && !tf) ? 256 : 128;
+  const int CG = (tile >= 2) ? 2 : 1;
   const int BN_CTA = BN / CG;
   const int BK = tf ? 32 : 64;
   const int CHUNK = BK;  // MN elements per 128-byte row (= BK for both element sizes)
@@ -199,7 +236,9 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   plan->tiles_m = static_cast<int>((d.M + 128 * CG - 1) / (128 * CG));
   plan->tiles_n = static_cast<int>((d.N + BN - 1) / BN);
   void* k = nullptr;
-  if (tile == 2)
+  if (tile == 3)
+    k = select_kernel_512(d.a_mn, d.b_mn, d.epilogue, &plan->smem);
+  else if (tile == 2)
     k = tf ? select_kernel<128, 2, true>(d.a_mn, d.b_mn, d.epilogue, &plan->smem)
            : select_kernel<256, 2, false>(d.a_mn, d.b_mn, d.epilogue, &plan->smem);
   else
@@ -216,9 +255,11 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
   auto map_a = [&](CUtensorMap* m, const void* p) {
     return d.a_mn ? make_tmap(m, p, tf, d.M, K, d.lda, CHUNK, BK, tf) : make_tmap(m, p, tf, K, d.M, d.lda, BK, 128);
   };
+  // K-major B boxes cover one piece of a CTA's B columns (128 rows; the 512-wide tile loads two)
+  const uint32_t b_box = tile == 3 ? BN_CTA / 2 : BN_CTA;
   auto map_b = [&](CUtensorMap* m, const void* p) {
     return d.b_mn ? make_tmap(m, p, tf, d.N, K, d.ldb, CHUNK, BK, tf)
-                  : make_tmap(m, p, tf, K, d.N, d.ldb, BK, BN_CTA);
+                  : make_tmap(m, p, tf, K, d.N, d.ldb, BK, b_box);
   };
   bool ok = map_a(&plan->tmA, d.A) && map_b(&plan->tmB, d.B);
   if (ok && tf) {

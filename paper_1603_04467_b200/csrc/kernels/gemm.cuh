@@ -50,7 +50,15 @@ struct GemmCfg {
   static constexpr int A_TILE = BM * BK * E;      // 16 KB
   static constexpr int B_TILE = BN_CTA * BK * E;  // 16 KB (BN_CTA = 128)
   static constexpr int STAGE_BYTES = NOPS * (A_TILE + B_TILE);
-  static constexpr int TMEM_COLS = 2 * BN;        // two accumulator buffers
+  // BN = 512 (bf16 CTA pair): the tile's accumulator is two N = 256 halves filling all 512
+  // TMEM columns (no second buffer); each half is handed to the epilogue / back to the MMA on
+  // its own barrier, so the next tile's first half starts while the epilogue drains the second.
+  // Each CTA loads its B columns as NH pieces of 128 (piece h feeds half h), so a pair tile
+  // reads 25 % fewer operand bytes per FLOP than two 256 x 256 tiles.
+  static constexpr int NH = BN > 256 ? 2 : 1;     // accumulator halves per tile
+  static constexpr int MMA_N = BN > 256 ? 256 : BN;
+  static constexpr int PIECE_COLS = BN_CTA / NH;  // B columns per piece (128)
+  static constexpr int TMEM_COLS = NH == 2 ? 512 : 2 * BN;  // two buffers, or the two halves of one
   // tile-id ring depth: the producer runs ~1 tile ahead of the MMA and the epilogue ~1 tile
   // behind it, so the ring must hold >= 3 ids or the producer stalls at tile boundaries
   static constexpr int SCHED_DEPTH = 4;
@@ -146,26 +154,27 @@ __device__ __forceinline__ void store_operand(float (&v)[32], void* hi_base, voi
   const bool full = gn + 32 <= N;
   if constexpr (!TF32) {
     // bf16 operand: RNE (reading A19), or — where the tensor crosses a device (f4 channel,
-    // reading A33) — the channel's 16-bit truncation code, which is a bf16 bit pattern
+    // reading A33) — the channel's 16-bit truncation code, which is a bf16 bit pattern.
+    // Packed pairwise (one cvt per two values); v is handed back as the stored values (the
+    // fused db column sums use them; dead and dropped by the compiler elsewhere)
+    uint32_t w[16];
 #pragma unroll
-    for (int j = 0; j < 32; ++j)
-      v[j] = trunc ? __uint_as_float(__float_as_uint(v[j]) & 0xFFFF0000u) : __bfloat162float(__float2bfloat16_rn(v[j]));
+    for (int e = 0; e < 16; ++e)
+      w[e] = trunc ? ((__float_as_uint(v[2 * e]) >> 16) | (__float_as_uint(v[2 * e + 1]) & 0xFFFF0000u))
+                   : pack_bf16x2(v[2 * e], v[2 * e + 1]);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(hi_base) + gm * ld + gn;
     if (full && vec == 2) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 16) {
-        uint32_t w[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) w[e] = pack_bf16x2(v[j + 2 * e], v[j + 2 * e + 1]);
-        st_v8(o + j, w, cs);
-      }
+      st_v8(o, w, cs);
+      st_v8(o + 16, w + 8, cs);
     } else if (full && vec) {
 #pragma unroll
       for (int j = 0; j < 32; j += 8)
-        st_once(reinterpret_cast<uint4*>(o + j),
-                make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]), pack_bf16x2(v[j + 4], v[j + 5]),
-                           pack_bf16x2(v[j + 6], v[j + 7])),
-                cs);
+        st_once(reinterpret_cast<uint4*>(o + j), make_uint4(w[j / 2], w[j / 2 + 1], w[j / 2 + 2], w[j / 2 + 3]), cs);
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j)
@@ -293,12 +302,15 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t full0 = (CG == 2) ? ptx::mapa_shared(full0_local, 0) : full0_local;
       const uint32_t s_tiles = ptx::smem_u32(tiles);
       // This CTA's (m0, n0) of tile t.
+      // n0 = this CTA's first B column of piece 0; piece p starts at n0 + p * (BN / NH)
       auto origin = [&](int t, int& m0, int& n0) {
         int tm, tn;
         tile_coords(t, args.tiles_m, args.tiles_n, args.group_m, tm, tn);
         m0 = tm * (BM * CG) + cta_rank * BM;
-        n0 = tn * BN + cta_rank * BN_CTA;
+        n0 = tn * BN + cta_rank * Cfg::PIECE_COLS;
       };
+      constexpr int PIECE_STRIDE = BN / Cfg::NH;              // global columns between pieces
+      constexpr int PIECE_BYTES = Cfg::PIECE_COLS * BK * Cfg::E;  // smem bytes of one piece
       // L2 prefetch cursor: walks the same (tile, k-block) sequence `pf` k-blocks ahead of
       // the loads, so the loads hit L2 instead of waiting out DRAM latency. It draws the tile
       // ids from the scheduler ring (one tile ahead of the loads, which take them from t_next).
@@ -318,8 +330,11 @@ __global__ void __launch_bounds__(256, 1)
             for (int i = 0; i < (A_MN ? BM / CHUNK : 1); ++i)
               ptx::tma_prefetch_2d(ma, A_MN ? (pm0 + CHUNK * i) : k0, A_MN ? k0 : pm0);
 #pragma unroll
-            for (int i = 0; i < (B_MN ? BN_CTA / CHUNK : 1); ++i)
-              ptx::tma_prefetch_2d(mb, B_MN ? (pn0 + CHUNK * i) : k0, B_MN ? k0 : pn0);
+            for (int pc = 0; pc < Cfg::NH; ++pc)
+#pragma unroll
+              for (int i = 0; i < (B_MN ? Cfg::PIECE_COLS / CHUNK : 1); ++i)
+                ptx::tma_prefetch_2d(mb, B_MN ? (pn0 + pc * PIECE_STRIDE + CHUNK * i) : k0,
+                                     B_MN ? k0 : pn0 + pc * PIECE_STRIDE);
           }
         }
         __syncwarp();
@@ -361,13 +376,16 @@ __global__ void __launch_bounds__(256, 1)
                   else ptx::tma_load_2d(dst, ma, fb, c0, c1);
                 }
 #pragma unroll
-                for (int i = 0; i < (B_MN ? BN_CTA / CHUNK : 1); ++i) {
-                  const uint32_t dst = sb + i * CHUNK_BYTES;
-                  const int c0 = B_MN ? (n0 + CHUNK * i) : k0;
-                  const int c1 = B_MN ? k0 : n0;
-                  if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, mb, fb, c0, c1);
-                  else ptx::tma_load_2d(dst, mb, fb, c0, c1);
-                }
+                for (int pc = 0; pc < Cfg::NH; ++pc)
+#pragma unroll
+                  for (int i = 0; i < (B_MN ? Cfg::PIECE_COLS / CHUNK : 1); ++i) {
+                    const uint32_t dst = sb + pc * PIECE_BYTES + i * CHUNK_BYTES;
+                    const int nn = n0 + pc * PIECE_STRIDE;
+                    const int c0 = B_MN ? (nn + CHUNK * i) : k0;
+                    const int c1 = B_MN ? k0 : nn;
+                    if constexpr (CG == 2) ptx::tma_load_2d_cg2(dst, mb, fb, c0, c1);
+                    else ptx::tma_load_2d(dst, mb, fb, c0, c1);
+                  }
               }
             }
           }
@@ -380,7 +398,7 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA; warp-uniform, one elected lane issues) =====================
     if (cta_rank == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc(BM * CG, BN, A_MN, B_MN, TF32);
+      constexpr uint32_t idesc = ptx::make_idesc(BM * CG, Cfg::MMA_N, A_MN, B_MN, TF32);
       // smem descriptors of stage 0; a stage / k step only moves the start address
       // (field [0,14) = addr >> 4, < 2^14 for any shared address, so plain adds never carry)
       auto mn_desc = [&](uint32_t addr) {
@@ -408,6 +426,44 @@ __global__ void __launch_bounds__(256, 1)
         const int t = next_tile(sslot, sph, true);
         if (t >= num_tiles) break;
         if (num_kb == 0) continue;
+        if constexpr (Cfg::NH == 2) {
+          // two N = 256 halves in TMEM columns [0, 256) and [256, 512); half 1 waits for the
+          // epilogue to hand it back only after half 0's first MMAs are issued
+          constexpr uint32_t HB = static_cast<uint32_t>((Cfg::PIECE_COLS * BK * Cfg::E) >> 4);  // piece offset
+          ptx::mbar_wait(ptx::smem_u32(&tempty[0]), acc_phase ^ 1);
+          ptx::tc_fence_after();
+          for (int kb = 0; kb < num_kb; ++kb) {
+            ptx::mbar_wait(ptx::smem_u32(&full[stage]), phase);
+            ptx::tc_fence_after();
+            const uint64_t soff = static_cast<uint64_t>((stage * STAGE_BYTES) >> 4);
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int k = 0; k < BK / KMMA; ++k)
+                ptx::mma_ss<CG, false>(tmem_base, a_desc0[0] + soff + k * KA_STEP, b_desc0[0] + soff + k * KB_STEP,
+                                       idesc, (kb == 0 && k == 0) ? 0u : 1u);
+            }
+            __syncwarp();
+            if (kb == 0) {
+              ptx::mbar_wait(ptx::smem_u32(&tempty[1]), acc_phase ^ 1);
+              ptx::tc_fence_after();
+            }
+            if (ptx::elect_one()) {
+#pragma unroll
+              for (int k = 0; k < BK / KMMA; ++k)
+                ptx::mma_ss<CG, false>(tmem_base + 256, a_desc0[0] + soff + k * KA_STEP,
+                                       b_desc0[0] + soff + HB + k * KB_STEP, idesc, (kb == 0 && k == 0) ? 0u : 1u);
+              ptx::mma_commit<CG>(ptx::smem_u32(&empty[stage]), 0x3);
+              if (kb == num_kb - 1) {
+                ptx::mma_commit<CG>(ptx::smem_u32(&tfull[0]), 0x3);
+                ptx::mma_commit<CG>(ptx::smem_u32(&tfull[1]), 0x3);
+              }
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          acc_phase ^= 1;
+          continue;
+        }
         // K is processed in chunks, each accumulated from zero into one of the two TMEM
         // buffers (bf16: one chunk per tile; 3xTF32: 128-wide K chunks summed in fp32 by the
         // epilogue, because the tensor core truncates when it accumulates, reading A25)
@@ -547,18 +603,47 @@ __global__ void __launch_bounds__(256, 1)
       const int gm = tm * (BM * CG) + cta_rank * BM + q * 32 + lane;
       const bool row_ok = gm < args.M;
       const uint32_t tmem_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
-      auto release_tmem = [&]() {  // hand the TMEM buffer back to the MMA warp
+      // the tile's bias, lane l holding column 32k + l of chunk k: loaded before the
+      // accumulator wait (its latency hides behind the mainloop), broadcast per chunk by shfl
+      constexpr bool HAS_BIAS = EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_RELU_LOSS;
+      float bl[HAS_BIAS ? BN / 32 : 1];
+      if constexpr (HAS_BIAS) {
+#pragma unroll
+        for (int k = 0; k < BN / 32; ++k) {
+          const int gn = tn * BN + k * 32 + lane;
+          bl[k] = gn < args.N ? __ldg(args.bias + gn) : 0.f;
+        }
+      }
+      auto hand_back = [&](int slot) {  // hand a TMEM buffer (or half) back to the MMA warp
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
           // relaxed: the reads it releases completed at tcgen05.wait::ld; a release.cluster
           // arrive would add a GPU-scope MEMBAR per TMEM hand-back (per 128-deep K chunk on
           // the 3xTF32 path)
-          if constexpr (CG == 2) ptx::mbar_arrive_cluster_relaxed(tempty_leader + acc * 8);
-          else ptx::mbar_arrive(ptx::smem_u32(&tempty[acc]));
+          if constexpr (CG == 2) ptx::mbar_arrive_cluster_relaxed(tempty_leader + slot * 8);
+          else ptx::mbar_arrive(ptx::smem_u32(&tempty[slot]));
         }
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+      };
+      auto release_tmem = [&]() {
+        if constexpr (Cfg::NH == 2) {  // (half 0 went back at the half switch)
+          hand_back(1);
+          acc_phase ^= 1;
+        } else {
+          hand_back(acc);
+          acc ^= 1;
+          if (acc == 0) acc_phase ^= 1;
+        }
+      };
+      // NH == 2: before chunk BN / 64 (the first of half 1) give half 0 back and wait for half 1
+      auto half_switch = [&](int c) {
+        if constexpr (Cfg::NH == 2) {
+          if (c == BN / 64) {
+            hand_back(0);
+            ptx::mbar_wait(ptx::smem_u32(&tfull[1]), acc_phase);
+            ptx::tc_fence_after();
+          }
+        }
       };
       // 3xTF32: the K chunks arrive one TMEM buffer at a time; sum them in fp32 (RN)
       float kacc[TF32 ? BN : 1];
@@ -583,6 +668,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_wait(ptx::smem_u32(&tfull[acc]), acc_phase);
         ptx::tc_fence_after();
         if (args.debug & 2) {  // profiling: hand the accumulator straight back
+          half_switch(BN / 64);
           release_tmem();
           continue;
         }
@@ -612,10 +698,62 @@ __global__ void __launch_bounds__(256, 1)
           for (int j = 0; j < 32; ++j) yv[j] = (gn + j < args.N) ? __ldg(yrow + j) : 0.f;
         }
       };
-      auto column_chunk = [&](int c, uint32_t (&r)[32], const float (&yv)[32]) {
+      // the chunk's streamed operand, loaded one chunk ahead of its use: the targets (loss
+      // seed), the bf16 Relu mask (dgrad) or the fp32 master weights (SGD apply) — on the
+      // vectorised full-chunk path; ragged chunks load inline in column_chunk
+      const bool pre_vec = EPI == EPI_RELUGRAD ? (!TF32 && args.vec_mask != 0)
+                                               : EPI == EPI_SGD_APPLY ? args.vec_out32 != 0 : false;
+      auto load_pre = [&](int c, float (&p)[32]) {
+        if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
+          load_y(c, p);
+        } else if constexpr (EPI == EPI_RELUGRAD && !TF32) {
+          const int gn = tn * BN + c * 32;
+          if (!(pre_vec && row_ok && gn + 32 <= args.N)) return;
+          const OpT* mrow = reinterpret_cast<const OpT*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
+          uint32_t mw16[16];
+          if (args.vec_mask == 2) {
+            ld_v8(mrow, ev, mw16);
+            ld_v8(mrow + 16, ev, mw16 + 8);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              const uint4 mv = ld_once(reinterpret_cast<const uint4*>(mrow + j), ev);
+              mw16[j / 2] = mv.x; mw16[j / 2 + 1] = mv.y; mw16[j / 2 + 2] = mv.z; mw16[j / 2 + 3] = mv.w;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) p[j] = __uint_as_float(mw16[j]);
+        } else if constexpr (EPI == EPI_SGD_APPLY) {
+          const int gn = tn * BN + c * 32;
+          if (!(pre_vec && row_ok && gn + 32 <= args.N)) return;
+          const float* w = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
+          if (args.vec_out32 == 2) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) ld_v8(w + j, ev, reinterpret_cast<uint32_t*>(p + j));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 w4 = ld_once(reinterpret_cast<const float4*>(w + j), ev);
+              p[j] = w4.x; p[j + 1] = w4.y; p[j + 2] = w4.z; p[j + 3] = w4.w;
+            }
+          }
+        } else {
+          (void)c;
+          (void)p;
+        }
+      };
+      auto column_chunk = [&](int c, uint32_t (&r)[32], const float (&yv)[32], float bias_lane) {
         const int gn = tn * BN + c * 32;
         const bool active = row_ok && gn < args.N;
         const bool full_chunk = gn + 32 <= args.N;
+        float bv[HAS_BIAS ? 32 : 1];  // this chunk's 32 bias values (all lanes)
+        if constexpr (HAS_BIAS) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bv[j] = __shfl_sync(0xffffffffu, bias_lane, j);
+        } else {
+          (void)bias_lane;
+          bv[0] = 0.f;
+        }
         if constexpr (EPI == EPI_F32) {
           if (active) {
             float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
@@ -782,34 +920,22 @@ __global__ void __launch_bounds__(256, 1)
           if (active) {
             float* w = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
             float v[32];
-            if (full_chunk && args.vec_out32 == 2) {
+            if (full_chunk && pre_vec) {  // W prefetched by load_pre
 #pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint32_t w8[8];
-                ld_v8(w + j, ev, w8);
+              for (int j = 0; j < 32; ++j) v[j] = __fsub_rn(yv[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
+              if (args.vec_out32 == 2) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[j + e] = u32_as_f32(w8[e]);
+                for (int j = 0; j < 32; j += 8) {
+                  uint32_t w8[8];
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) w8[e] = __float_as_uint(v[j + e]);
+                  st_v8(w + j, w8, ev);
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                  st_once(reinterpret_cast<float4*>(w + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]), ev);
               }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __fsub_rn(v[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint32_t w8[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) w8[e] = __float_as_uint(v[j + e]);
-                st_v8(w + j, w8, ev);
-              }
-            } else if (full_chunk && args.vec_out32) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 w4 = ld_once(reinterpret_cast<const float4*>(w + j), ev);
-                v[j] = w4.x; v[j + 1] = w4.y; v[j + 2] = w4.z; v[j + 3] = w4.w;
-              }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __fsub_rn(v[j], __fmul_rn(args.sgd_lr, u32_as_f32(r[j])));
-#pragma unroll
-              for (int j = 0; j < 32; j += 4)
-                st_once(reinterpret_cast<float4*>(w + j), make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]), ev);
             } else {
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
@@ -824,17 +950,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         } else if constexpr (EPI == EPI_BIAS_RELU) {
           if (active) {
-            float v[32], bv[32];
-            if (full_chunk && args.vec_bias) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + gn + j));
-                bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) bv[j] = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
-            }
+            float v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const float z = __fadd_rn(u32_as_f32(r[j]), bv[j]);
@@ -866,17 +982,9 @@ __global__ void __launch_bounds__(256, 1)
               const OpT* mrow = reinterpret_cast<const OpT*>(args.mask) + static_cast<int64_t>(gm) * args.ldm + gn;
               if (full_chunk && args.vec_mask) {
                 if constexpr (!TF32) {
-                  uint32_t mw16[16];  // the 32 bf16 mask values of this chunk
-                  if (args.vec_mask == 2) {
-                    ld_v8(mrow, ev, mw16);
-                    ld_v8(mrow + 16, ev, mw16 + 8);
-                  } else {
+                  uint32_t mw16[16];  // the 32 bf16 mask values of this chunk (prefetched by load_pre)
 #pragma unroll
-                    for (int j = 0; j < 32; j += 8) {
-                      const uint4 mv = ld_once(reinterpret_cast<const uint4*>(mrow + j), ev);
-                      mw16[j / 2] = mv.x; mw16[j / 2 + 1] = mv.y; mw16[j / 2 + 2] = mv.z; mw16[j / 2 + 3] = mv.w;
-                    }
-                  }
+                  for (int j = 0; j < 16; ++j) mw16[j] = __float_as_uint(yv[j]);
 #pragma unroll
                   for (int j = 0; j < 32; j += 8) {
                     const uint32_t* mw = mw16 + j / 2;
@@ -905,17 +1013,6 @@ __global__ void __launch_bounds__(256, 1)
               }
             } else {  // EPI_BIAS_RELU_LOSS: a = relu(acc + b); loss seed (reading A2, A10, A20)
               float* o32 = args.out_f32 ? args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn : nullptr;
-              float bv[32];
-              if (full_chunk && args.vec_bias) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(args.bias + gn + j));
-                  bv[j] = b4.x; bv[j + 1] = b4.y; bv[j + 2] = b4.z; bv[j + 3] = b4.w;
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) bv[j] = (gn + j < args.N) ? __ldg(args.bias + gn + j) : 0.f;
-              }
               float av[32];
               float part = 0.f;  // this chunk's loss contribution (fp32), folded into loss_acc (fp64)
 #pragma unroll
@@ -971,48 +1068,64 @@ __global__ void __launch_bounds__(256, 1)
         __syncwarp();
       };
       if constexpr (TF32) {
-        // (the K-chunk sums already hold 128 registers: one target buffer, loaded per chunk)
+        // (the K-chunk sums already hold 128 registers: one operand buffer, loaded per chunk)
 #pragma unroll
         for (int c = 0; c < BN / 32; ++c) {
-          float yv[32];
-          if constexpr (EPI == EPI_BIAS_RELU_LOSS) load_y(c, yv);
+          float pre[32];
+          load_pre(c, pre);
           uint32_t r[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(kacc[c * 32 + j]);
-          column_chunk(c, r, yv);
+          column_chunk(c, r, pre, bl[HAS_BIAS ? c : 0]);
         }
       } else {
-        auto tmem_chunk = [&](int c, uint32_t (&r)[32]) {
+        // Software-pipelined and rolled (an unrolled epilogue overflows the instruction
+        // cache): chunk c + 1's TMEM load and streamed operand are in flight while chunk c is
+        // processed, so the drain runs at issue rate, not at TMEM + DRAM latency per chunk —
+        // with the 512-wide tile the MMA waits on this drain at every tile boundary.
+        auto tmem_issue = [&](int c, uint32_t (&r)[32]) {
           if (num_kb > 0) {
+            half_switch(c);
             ptx::tmem_ld_32x32b_x32(tmem_row + acc * BN + c * 32, r);
-            ptx::tmem_ld_wait();
+          }
+        };
+        auto tmem_land = [&](uint32_t (&r)[32]) {
+          if (num_kb > 0) {
+            ptx::tmem_ld_wait_regs(r);
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = 0u;  // K == 0: the empty sum
           }
         };
-        if constexpr (EPI == EPI_BIAS_RELU_LOSS) {
-          // rolled (an unrolled epilogue overflows the instruction cache); the next chunk's
-          // targets are in flight while this chunk is processed
-          float ycur[32], ynext[32];
-          load_y(0, ycur);
+        // two register sets, alternating roles chunk by chunk (the loop body is one even and
+        // one odd chunk, so no copies between them)
+        float pa[32], pb[32];
+        uint32_t ra[32], rb[32];
+        auto step = [&](int c, uint32_t (&rcur)[32], float (&pcur)[32], uint32_t (&rnext)[32], float (&pnext)[32],
+                        float bcur) {
+          const bool more = c + 1 < BN / 32;
+          if (more) {
+            load_pre(c + 1, pnext);
+            tmem_issue(c + 1, rnext);
+          }
+          column_chunk(c, rcur, pcur, bcur);
+          if (more) tmem_land(rnext);
+        };
+        load_pre(0, pa);
+        tmem_issue(0, ra);
+        tmem_land(ra);
+        static_assert((BN / 32) % 2 == 0, "chunk pairs");
 #pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            if (c + 1 < BN / 32) load_y(c + 1, ynext);
-            uint32_t r[32];
-            tmem_chunk(c, r);
-            column_chunk(c, r, ycur);
+        for (int c = 0; c < BN / 32; c += 2) {
+          float b0 = 0.f, b1 = 0.f;
+          if constexpr (HAS_BIAS) {
+            b0 = bl[0];
+            b1 = bl[1];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) ycur[j] = ynext[j];
+            for (int k = 0; k + 2 < BN / 32; ++k) bl[k] = bl[k + 2];
           }
-        } else {
-          float ydummy[1][32];
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            tmem_chunk(c, r);
-            column_chunk(c, r, ydummy[0]);
-          }
+          step(c, ra, pa, rb, pb, b0);
+          step(c + 1, rb, pb, ra, pa, b1);
         }
         if (num_kb > 0) release_tmem();
       }

@@ -39,12 +39,16 @@ def main():
     vp = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
     flops = 2.0 * b * w * w
 
+    tile = [0]
+
     def ours(M, N, K, Ad, am, Bd, bm, epi, out=None, o32=None, mask=None, bias_=None):
+        t = tile[0]
+
         def f():
             D.check(D.dflow_gemm_bf16(M, N, K, vp(Ad), Ad.stride(0), am, vp(Bd), Bd.stride(0), bm, epi, vp(out),
                                       out.stride(0) if out is not None else 0, vp(o32),
                                       o32.stride(0) if o32 is not None else 0, vp(bias_), vp(mask),
-                                      mask.stride(0) if mask is not None else 0, 0, sp))
+                                      mask.stride(0) if mask is not None else 0, t, sp))
         return f
 
     def split_wgrad(P):
@@ -70,7 +74,12 @@ def main():
     }
     res = {"shape": [b, w]}
     for v in args.variants.split(","):
-        base, _, dbg = v.partition("_d")
+        # suffix _t<k>: force tile config k (3 = the 256 x 512 pair tile); _d<k>: debug bits
+        vv, _, tsel = v.partition("_t")
+        tile[0] = int(tsel) if tsel.isdigit() else 0
+        if not tsel.isdigit():
+            vv = v
+        base, _, dbg = vv.partition("_d")
         if base.endswith("_cublas") or v.endswith("_cublas"):
             base, dbg = v, ""
         os.environ["DFLOW_GEMM_DEBUG"] = dbg or "0"

@@ -109,7 +109,7 @@ SHAPES = [(128, 128, 64), (100, 100, 784), (257, 300, 200), (256, 1024, 784), (5
 LAYOUTS = [(0, 1, D.EPI_F32), (0, 0, D.EPI_F32), (1, 1, D.EPI_F32)]
 
 
-@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("tile", [1, 2, 3])
 @pytest.mark.parametrize("a_mn,b_mn,epi", LAYOUTS)
 @pytest.mark.parametrize("M,N,K", SHAPES)
 def test_gemm_layouts_exact_integers(M, N, K, a_mn, b_mn, epi, tile):
@@ -123,7 +123,7 @@ def test_gemm_layouts_exact_integers(M, N, K, a_mn, b_mn, epi, tile):
     assert np.array_equal(out32.cpu().numpy()[:, :N], ref.astype(np.float32))
 
 
-@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("tile", [1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(300, 260, 520), (1024, 1024, 4096)])
 def test_gemm_random_floats_tolerance(M, N, K, tile):
     g = rng(7)
@@ -137,7 +137,7 @@ def test_gemm_random_floats_tolerance(M, N, K, tile):
         assert np.all(err <= 2e-6 * bound + 1e-30), (a_mn, b_mn, float(np.max(err / (bound + 1e-30))))
 
 
-@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("tile", [1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(300, 260, 520), (100, 100, 784), (512, 512, 512)])
 def test_gemm_epilogue_trunc16(M, N, K, tile):
     g = rng(8)
@@ -148,7 +148,7 @@ def test_gemm_epilogue_trunc16(M, N, K, tile):
     assert np.array_equal(out.cpu().numpy()[:, :N].view(np.uint16), truncate16(ref))
 
 
-@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("tile", [1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(300, 260, 520), (100, 100, 784), (512, 1024, 256)])
 def test_gemm_epilogue_bias_relu(M, N, K, tile):
     g = rng(9)
@@ -165,7 +165,7 @@ def test_gemm_epilogue_bias_relu(M, N, K, tile):
     assert np.array_equal(out.float().cpu().numpy()[:, :N], _bf16_round(a))
 
 
-@pytest.mark.parametrize("tile", [1, 2])
+@pytest.mark.parametrize("tile", [1, 2, 3])
 @pytest.mark.parametrize("M,N,K", [(300, 260, 520), (256, 784, 1024), (512, 512, 512)])
 def test_gemm_epilogue_relugrad(M, N, K, tile):
     g = rng(10)
