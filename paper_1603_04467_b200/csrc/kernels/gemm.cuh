@@ -747,9 +747,17 @@ __global__ void __launch_bounds__(256, 1)
         const bool active = row_ok && gn < args.N;
         const bool full_chunk = gn + 32 <= args.N;
         float bv[HAS_BIAS ? 32 : 1];  // this chunk's 32 bias values (all lanes)
+        // profiling (debug 16): the output stores are skipped (issue and L1 cost of the
+        // drain without them); debug 32: the bias broadcast is skipped
+        const bool skip_st = (args.debug & 16) != 0;
         if constexpr (HAS_BIAS) {
+          if (args.debug & 32) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) bv[j] = __shfl_sync(0xffffffffu, bias_lane, j);
+            for (int j = 0; j < 32; ++j) bv[j] = bias_lane;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) bv[j] = __shfl_sync(0xffffffffu, bias_lane, j);
+          }
         } else {
           (void)bias_lane;
           bv[0] = 0.f;
@@ -956,7 +964,7 @@ __global__ void __launch_bounds__(256, 1)
               const float z = __fadd_rn(u32_as_f32(r[j]), bv[j]);
               v[j] = (z < 0.f) ? 0.f : z;  // Relu; NaN propagates (non-finite guard)
             }
-            if (args.out_f32 != nullptr) {
+            if (args.out_f32 != nullptr && !skip_st) {
               float* o = args.out_f32 + static_cast<int64_t>(gm) * args.ldo32 + gn;
               if (full_chunk && args.vec_out32) {
 #pragma unroll
@@ -968,7 +976,7 @@ __global__ void __launch_bounds__(256, 1)
                   if (gn + j < args.N) o[j] = v[j];
               }
             }
-            if (args.out != nullptr)
+            if (args.out != nullptr && !skip_st)
               store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out,
                                   args.trunc_out != 0, ev);
           }
@@ -1045,7 +1053,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
               }
             }
-            store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out, false, ev);
+            if (!skip_st) store_operand<TF32>(v, args.out, args.out2, args.ldo, gm, gn, args.N, args.vec_out, false, ev);
           }
           if (args.colsum_ws != nullptr) {
             // transpose-reduce: after 5 butterfly steps lane l holds the sum over this
