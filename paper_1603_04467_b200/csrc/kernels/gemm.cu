@@ -209,10 +209,8 @@ cudaError_t gemm_prepare(const GemmDesc& d, int num_sms, GemmPlan* plan) {
     // at a higher power-capped clock, but its single TMEM accumulator exposes the epilogue
     // drain at every tile boundary: the N = 1 step is 5 % slower with it everywhere and
     // unchanged with it on the weight gradient only
-    static const int wide = [] {
-      const char* e = getenv("DFLOW_GEMM_TILE512");
-      return e ? atoi(e) : 0;
-    }();
+    const char* wide_env = getenv("DFLOW_GEMM_TILE512");  // read per plan, like the raster knobs
+    const int wide = wide_env ? atoi(wide_env) : 0;
     int dummy = 0;
     const bool wgrad_kind = d.a_mn && d.b_mn;
     if ((wide == 1 || (wide == 2 && wgrad_kind)) && tile == 2 && !d.tf32 &&

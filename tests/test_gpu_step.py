@@ -348,6 +348,32 @@ def test_raster_group_leaves_results_bitwise(monkeypatch):
         assert np.array_equal(a, b)
 
 
+def test_wide_tile_knob_leaves_results_bitwise(monkeypatch):
+    # DFLOW_GEMM_TILE512=1 (off by default) runs every GEMM of the step on the
+    # 256 x 512 pair tile (fused loss seed, ReluGrad + db partials, fused SGD included): each
+    # output element still accumulates its K products in the same order, so W and b after a
+    # step are bit-identical; the cost's fp64 partials are summed per tile, so only the sum
+    # order of the loss changes.
+    w = with_batch(C3, 2048)
+    Ws, bs = init_params(w)
+    X, Y = batch(w)
+    out = []
+    for wide in ("0", "1"):
+        monkeypatch.setenv("DFLOW_GEMM_TILE512", wide)
+        run = Run(w.dims, w.loss, w.lr, rows=2048)
+        try:
+            run.assign(Ws, bs)
+            loss = run.step(_dev(X), _dev(Y))
+            Wg, bg = run.read()
+            out.append((loss, Wg, bg))
+        finally:
+            run.close()
+    (l0, W0, b0), (l1, W1, b1) = out
+    assert abs(l0 - l1) <= 1e-6 * abs(l0)
+    for a, b in zip(W0 + b0, W1 + b1):
+        assert np.array_equal(a, b)
+
+
 def test_loss_bitwise_reproducible_under_dynamic_scheduler():
     """The cost is summed from one fp64 partial per (tile, CTA, epilogue warp) in a fixed
     order, so repeated forwards give the same bits even though the dynamic tile scheduler
